@@ -1,0 +1,307 @@
+"""Benchmark: training chars/s of the paper's 4096-d mLSTM step (seq 256, 256 rows/GPU, mixed fp16/fp32
+with dynamic loss scaling) on N B200s, data parallel (BASELINE.json `metric`, configs[2]).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3|C1|C2|C5]
+  N > 1: python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+Rank 0 prints ONE JSON line.  `value` = N*B*T / (max over ranks of the CUDA-event time of K steps)/K,
+inputs resident in HBM.  `e2e` = the same metric through mlstm_train_step_host (pinned host bytes
+H2D + result D2H inside the timed region).  `roofline` = the dominant GEMM phase's algorithmic
+FLOP/s vs MEASURED_PEAKS.json.  `cpu_baseline` = the fp64 oracle on a bounded sample (rank 0, N=1).
+--impl reference times that oracle alone (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+if __name__ == "__main__":  # oracle / numpy threads = all host cores (set before numpy loads)
+    _n = str(len(os.sched_getaffinity(0)))
+    for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ.setdefault(_v, _n)
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training chars/sec (4096-d mLSTM, seq 256) at 1/2/4/8 B200; tensor-pipe %"
+CONFIGS = {
+    # name: (h, e, B per GPU, T, description)
+    "C1": (64, 64, 4, 16, "tiny mLSTM h=64 e=64, seq 16, batch 4/GPU"),
+    "C2": (1024, 64, 128, 64, "mLSTM h=1024 e=64, seq 64, batch 128/GPU"),
+    "C3": (4096, 64, 256, 256, "paper model: mLSTM h=4096 e=64, seq 256, batch 256/GPU, fp16/fp32 mixed, "
+                               "dynamic loss scaling"),
+    "C5": (8192, 64, 128, 256, "8192-d mLSTM e=64, seq 256, batch 128/GPU, fp16/fp32 mixed"),
+}
+DEVSTATE_BYTES = 56  # the device scalar block the step copies back (loss, alpha, lr, skip, it, tau)
+
+
+def flops_per_char(h, e):
+    """6 (5h^2 + 5he + 256h) -- fwd, dW and dX of every matmul."""
+    return 6.0 * (5 * h * h + 5 * h * e + 256 * h)
+
+
+def phase_flops(h, e, B, T):
+    """Algorithmic FLOPs of each GEMM phase of one step (per rank)."""
+    BT = B * T
+    return {
+        "fwd_rec": 2.0 * BT * 5 * h * h,                                   # W_mh h, W_h m per char
+        "bwd_rec": 2.0 * BT * 5 * h * h - 2.0 * B * h * h,                 # dZ W_h, dA W_mh (t>0)
+        "wgrad": 2.0 * BT * (5 * h * h + 5 * h * e + 256 * h),             # dW_h, dW_mh, dW_x, dW_mx, dW_dec
+        "decoder": 2.0 * BT * 256 * h,
+        "dhdec": 2.0 * BT * 256 * h,
+    }
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["bf16_tflops"], d["bf16_tflops_sustained"], d["hbm_gbs"], "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(h, e, seconds_hint=15.0):
+    """The fp64 oracle as it stands, on a bounded sample of the same workload (same h, e, T=128 window,
+    B rows chosen so the sample is ~10-30 s of CPU work): forward, BPTT and Adam."""
+    from oracle import mlstm_oracle as O
+    from synth import bytestream
+    cores = len(os.sched_getaffinity(0))
+    P = O.init_params(h, e, 0x5EED)
+    theta = O.flatten(P)
+    T = 128 if h >= 2048 else 64
+    B = 1
+    # calibrate on one row, then scale the row count toward the time hint
+    t0 = time.perf_counter()
+    by = bytestream.window(np.arange(B), 0, T)
+    z = np.zeros((B, h))
+    O.loss_and_grads(P, by, z, z)
+    dt1 = time.perf_counter() - t0
+    B = int(max(1, min(64, seconds_hint / max(dt1, 1e-3))))
+    by = bytestream.window(np.arange(B), 0, T)
+    z = np.zeros((B, h))
+    t0 = time.perf_counter()
+    _, g, _, _ = O.loss_and_grads(P, by, z, z)
+    st = O.AdamState(np.zeros_like(theta), np.zeros_like(theta))
+    O.adam_apply(theta, O.flatten(g), st, 3e-3)
+    dt = time.perf_counter() - t0
+    return {"value": B * T / dt, "unit": "chars/s", "cores": cores, "kind": "oracle",
+            "sample": f"fp64 NumPy oracle, h={h} e={e}, {B} rows x T={T} window (forward, BPTT, Adam), "
+                      f"{dt:.1f} s on {cores} host threads"}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    h, e, B, T, desc = CONFIGS[args.config]
+    # each "step" is one bounded sample of the workload on the host cores
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(h, e, seconds_hint=args.ref_seconds)
+        if i >= args.warmup:
+            vals.append(r["value"])
+    v = float(np.median(vals))
+    ms = (B * T) / v * 1e3
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "chars/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "global_batch": B * args.gpus, "seq_len": T, "parallelism": f"dp{args.gpus}"},
+        "cpu_baseline": {**r, "value": v},
+        "e2e": {"value": v, "unit": "chars/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1808_01371_b200 as M
+    from synth import bytestream
+
+    rank, local, world = dist_env()
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    h, e, B, T, desc = CONFIGS[args.config]
+    cfg = M.mlstm_default_config(hidden=h, embed=e, batch=B, seq_len=T, precision=M.MLSTM_MIXED)
+    nid = None
+    if world > 1:
+        t = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(M.mlstm_nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        nid = bytes(t.cpu().numpy().tobytes())
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        model = M.MLSTM(cfg, rank=rank, world=world, nccl_id=nid, stream=stream)
+    nsteps = args.warmup + args.steps
+    rows = np.arange(rank * B, (rank + 1) * B)
+    windows = bytestream.windows(rows, 0, nsteps + (0 if args.no_e2e else args.steps), T)
+    dev = torch.from_numpy(windows[:nsteps].copy()).to(f"cuda:{local}")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for i in range(args.warmup):
+        model.train_step(dev[i])
+    launches = model.launches_per_step()
+    model.profile(True)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    results = []
+    for i in range(args.warmup, nsteps):
+        results.append(model.train_step(dev[i]))
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    phases = model.phase_times()
+    model.profile(False)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / args.steps
+    value = world * B * T / (ms_step / 1e3)
+
+    # end to end through the public host entry point (pinned host bytes in, result struct out)
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.from_numpy(windows[nsteps:].copy()).pin_memory()
+        host = pinned.numpy()
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.steps):
+            model.train_step_host(host[i])
+        t1.record(stream)
+        barrier()
+        ems = t0.elapsed_time(t1)
+        if world > 1:
+            tt = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": world * B * T / (ems / args.steps / 1e3), "unit": "chars/s",
+               "h2d_bytes_per_step": B * (T + 1), "d2h_bytes_per_step": DEVSTATE_BYTES}
+
+    if rank != 0:
+        return
+    # roofline of the dominant GEMM phase (tensor bound; fp16 peak == bf16 peak, dense)
+    burst, sustained, hbm, src = load_peaks()
+    pf = phase_flops(h, e, B, T)
+    gem = {k: phases[k] for k in pf if k in phases}
+    dom = max(gem, key=lambda k: gem[k][0])
+    dom_ms = gem[dom][0] / args.steps
+    dom_launches = gem[dom][1]
+    achieved = pf[dom] / (dom_ms / 1e3) / 1e12
+    roof = {"bound": "tensor", "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
+            "frac": achieved / sustained, "traffic": None, "peak_source": f"{src} bf16_tflops_sustained",
+            "kernel": f"gemm_tc_kernel ({dom} phase: {dom_launches} launches/step, "
+                      f"{pf[dom] / dom_launches / 1e9:.2f} GFLOP per launch avg, "
+                      f"{dom_ms / dom_launches * 1e3:.1f} us per launch avg)"}
+    whole = flops_per_char(h, e) * world * B * T / (ms_step / 1e3) / 1e12 / world
+    line = {
+        "metric": METRIC, "value": value, "unit": "chars/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16 (fp32 accumulate, fp32 masters)", "data": "synthetic",
+        "config": {"workload": desc, "global_batch": world * B, "seq_len": T, "parallelism": f"dp{world}",
+                   "l2": "no flush: per-step working set (~11 GB) >> 126 MB L2"},
+        "roofline": roof,
+        "step_tflops_per_gpu": whole, "step_frac_of_sustained_peak": whole / sustained,
+        "phases_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in phases.items()},
+        "clocks": clk, "e2e": e2e, "gpu_launches": launches * args.steps,
+        "loss_first_last": [results[0]["loss_nats"], results[-1]["loss_nats"]],
+        "skipped_steps": int(sum(r["skipped"] for r in results)),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(h, e)
+    print(json.dumps(line), flush=True)
+    model.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

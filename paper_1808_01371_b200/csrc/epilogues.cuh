@@ -1,0 +1,222 @@
+// epilogues.cuh -- the fused GEMM epilogues of the step.
+//
+// Every functor is called by one thread for one accumulator row and 64 consecutive columns:
+//   (row, col0, v[0..63]) with v = fp32 accumulator values.  Rows of the per-timestep GEMMs are
+//   batch rows b; columns are hidden units (N = h) or internal gate rows (N = 4h).
+#pragma once
+#include "net.cuh"
+
+namespace mlstm {
+
+// (a) input-projection table: tab[v][:] = [W_mx E[v] | W_x E[v]]  (the per-token input GEMM of
+// every timestep, done once per step for the 256 possible bytes; gathered by byte below).
+template <typename S>
+struct EpiTab {
+  Net<S> n;
+  __device__ __forceinline__ void operator()(int row, int col0, float (&v)[64]) const {
+    float* dst = n.tab + (long)row * 5 * n.h + col0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) st16(dst + 16 * q, v + 16 * q);
+  }
+};
+
+// (b) forward GEMM 1, A_t = H_{t-1} W_mh^T:  m_t = mx_t * a_t  (multiplicative intermediate).
+template <typename S>
+struct EpiF1 {
+  Net<S> n;
+  int t;
+  __device__ __forceinline__ void operator()(int b, int col0, float (&v)[64]) const {
+    const float* mx = n.tab + (long)n.byte_at(b, t) * 5 * n.h + col0;
+    S* mrow = n.Mscr + (long)b * n.h + col0;
+    S* arow = n.Astash + ((long)t * n.B + b) * n.h + col0;
+    const long kc = n.kcol(t, b);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float x[16], m[16];
+      ld16(mx + 16 * q, x);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) m[i] = x[i] * v[16 * q + i];
+      st16(mrow + 16 * q, m);
+      st16(arow + 16 * q, v + 16 * q);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) n.MT[(long)(col0 + 16 * q + i) * n.ldK + kc] = to_s<S>(m[i]);
+    }
+  }
+};
+
+// (b) forward GEMM 2, Z_t = M_t W_h^T (+ W_x x_t + b): gates, cell update, hidden state.
+template <typename S>
+struct EpiF2 {
+  Net<S> n;
+  int t;
+  __device__ __forceinline__ void operator()(int b, int col0, float (&v)[64]) const {
+    const int h = n.h;
+    const int j0 = (col0 >> 6) * 16;
+    const float* xz = n.tab + (long)n.byte_at(b, t) * 5 * h + h + col0;
+    const float* bias = n.master + n.po.b;
+    float xv[64];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ld16(xz + 16 * q, xv + 16 * q);
+    float cprev[16];
+    ld16(n.Crm + ((long)t * n.B + b) * h + j0, cprev);
+    float gi[16], gf[16], go[16], gu[16], cv[16], hv[16];
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      const int j = j0 + jj;
+      const float zi = v[jj] + xv[jj] + bias[j];
+      const float zf = v[16 + jj] + xv[16 + jj] + bias[h + j];
+      const float zo = v[32 + jj] + xv[32 + jj] + bias[2 * h + j];
+      const float zu = v[48 + jj] + xv[48 + jj] + bias[3 * h + j];
+      gi[jj] = sigmoidf_(zi);
+      gf[jj] = sigmoidf_(zf);
+      go[jj] = sigmoidf_(zo);
+      gu[jj] = tanhf(zu);
+      cv[jj] = gf[jj] * cprev[jj] + gi[jj] * gu[jj];  // c_t = f c_{t-1} + i u   (fp32)
+      hv[jj] = go[jj] * tanhf(cv[jj]);                 // h_t = o tanh(c_t)
+    }
+    S* grow = n.Gates + ((long)t * n.B + b) * 4 * h + col0;
+    st16(grow, gi);
+    st16(grow + 16, gf);
+    st16(grow + 32, go);
+    st16(grow + 48, gu);
+    st16(n.Hrm + ((long)(t + 1) * n.B + b) * h + j0, hv);
+    st16(n.Crm + ((long)(t + 1) * n.B + b) * h + j0, cv);
+    const long kc = n.kcol(t + 1, b);
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) n.HT[(long)(j0 + jj) * n.ldH + kc] = to_s<S>(hv[jj]);
+  }
+};
+
+// (d) decoder logits Y = H W_dec^T + b_dec, fp32 ("operating on FP32 logits").
+template <typename S>
+struct EpiY {
+  Net<S> n;
+  __device__ __forceinline__ void operator()(int row, int col0, float (&v)[64]) const {
+    const float* bd = n.master + n.po.bdec + col0;
+    float* dst = n.Y + (long)row * 256 + col0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float o[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i] = v[16 * q + i] + bd[16 * q + i];
+      st16(dst + 16 * q, o);
+    }
+  }
+};
+
+// dH from the decoder: dH_dec = dY W_dec.
+template <typename S>
+struct EpiDHdec {
+  Net<S> n;
+  __device__ __forceinline__ void operator()(int row, int col0, float (&v)[64]) const {
+    float* dst = n.dHdec + (long)row * n.h + col0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) st16(dst + 16 * q, v + 16 * q);
+  }
+};
+
+// (c-1) backward gate step for timestep s and 16 units j0..j0+15 of row b, given dH (the sum of
+// the decoder and recurrent contributions).  TBTT: dC carry starts at zero for s = T-1.
+template <typename S>
+__device__ __forceinline__ void gate_bwd16(const Net<S>& n, int s, int b, int j0, const float* dh) {
+  const int h = n.h;
+  const long gofs = ((long)s * n.B + b) * 4 * h + (long)(j0 >> 4) * 64;
+  float gi[16], gf[16], go[16], gu[16], c[16], cp[16], dcn[16];
+  ld16(n.Gates + gofs, gi);
+  ld16(n.Gates + gofs + 16, gf);
+  ld16(n.Gates + gofs + 32, go);
+  ld16(n.Gates + gofs + 48, gu);
+  ld16(n.Crm + ((long)(s + 1) * n.B + b) * h + j0, c);
+  ld16(n.Crm + ((long)s * n.B + b) * h + j0, cp);
+  ld16(n.dC + (long)b * h + j0, dcn);
+  float dzi[16], dzf[16], dzo[16], dzu[16], dcnew[16];
+#pragma unroll
+  for (int jj = 0; jj < 16; ++jj) {
+    const float k = tanhf(c[jj]);
+    const float i = gi[jj], f = gf[jj], o = go[jj], u = gu[jj];
+    dzo[jj] = dh[jj] * k * o * (1.f - o);
+    const float dc = dcn[jj] + dh[jj] * o * (1.f - k * k);
+    dzi[jj] = dc * u * i * (1.f - i);
+    dzf[jj] = dc * cp[jj] * f * (1.f - f);
+    dzu[jj] = dc * i * (1.f - u * u);
+    dcnew[jj] = dc * f;
+  }
+  st16(n.dC + (long)b * h + j0, dcnew);
+  S* zrow = n.dZscr + (long)b * 4 * h + (long)(j0 >> 4) * 64;
+  st16(zrow, dzi);
+  st16(zrow + 16, dzf);
+  st16(zrow + 32, dzo);
+  st16(zrow + 48, dzu);
+  const long kc = n.kcol(s, b);
+  const long r0 = (long)h + (long)(j0 >> 4) * 64;
+#pragma unroll
+  for (int jj = 0; jj < 16; ++jj) {
+    n.dGT[(r0 + jj) * n.ldK + kc] = to_s<S>(dzi[jj]);
+    n.dGT[(r0 + 16 + jj) * n.ldK + kc] = to_s<S>(dzf[jj]);
+    n.dGT[(r0 + 32 + jj) * n.ldK + kc] = to_s<S>(dzo[jj]);
+    n.dGT[(r0 + 48 + jj) * n.ldK + kc] = to_s<S>(dzu[jj]);
+  }
+}
+
+// (c-1) backward GEMM 1, dM_t = dZ_t W_h:  dA = dM * mx,  dMX = dM * a.
+template <typename S>
+struct EpiB1 {
+  Net<S> n;
+  int t;
+  __device__ __forceinline__ void operator()(int b, int col0, float (&v)[64]) const {
+    const float* mx = n.tab + (long)n.byte_at(b, t) * 5 * n.h + col0;
+    const S* arow = n.Astash + ((long)t * n.B + b) * n.h + col0;
+    S* darow = n.dAscr + (long)b * n.h + col0;
+    const long kc = n.kcol(t, b);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float x[16], a[16], da[16], dmx[16];
+      ld16(mx + 16 * q, x);
+      ld16(arow + 16 * q, a);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        da[i] = v[16 * q + i] * x[i];
+        dmx[i] = v[16 * q + i] * a[i];
+      }
+      st16(darow + 16 * q, da);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const long r = col0 + 16 * q + i;
+        n.dAT[r * n.ldK + kc] = to_s<S>(da[i]);
+        n.dGT[r * n.ldK + kc] = to_s<S>(dmx[i]);
+      }
+    }
+  }
+};
+
+// (c-1) backward GEMM 2, dH_rec = dA_t W_mh, fused with the gate backward of step s = t-1.
+template <typename S>
+struct EpiB2 {
+  Net<S> n;
+  int s;
+  __device__ __forceinline__ void operator()(int b, int col0, float (&v)[64]) const {
+    const float* dhd = n.dHdec + ((long)s * n.B + b) * n.h + col0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float dh[16];
+      ld16(dhd + 16 * q, dh);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) dh[i] += v[16 * q + i];
+      gate_bwd16(n, s, b, col0 + 16 * q, dh);
+    }
+  }
+};
+
+// (c-2) split-K partial of a weight-gradient GEMM: part[z][row][col] (fp32).
+struct EpiPartial {
+  float* part;
+  long ldo;
+  long split_stride;
+  __device__ __forceinline__ void operator()(int row, int col0, float (&v)[64]) const {
+    float* dst = part + (long)blockIdx.z * split_stride + (long)row * ldo + col0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) st16(dst + 16 * q, v + 16 * q);
+  }
+};
+
+}  // namespace mlstm

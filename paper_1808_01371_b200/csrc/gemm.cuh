@@ -1,0 +1,192 @@
+// gemm.cuh -- the two GEMM engines every contraction of the step runs on.
+//
+//   D[M x N] = A[M x K] . B[N x K]^T   (both operands K-major, i.e. row-major with K contiguous),
+//   fp32 accumulation, result handed to a fused epilogue functor 64 columns at a time:
+//       epi(row, col0, float (&v)[64])   with v[i] = D[row][col0 + i].
+//
+// * gemm_tc_kernel (mixed precision, fp16 operands): TMA (128B swizzle) -> multi-stage mbarrier
+//   ring in shared memory -> single-thread tcgen05.mma (M=128, N=BN, K=16) into a TMEM fp32
+//   accumulator -> 4 epilogue warps tcgen05.ld their 32 TMEM lanes (one accumulator row per
+//   thread).  Warp roles: warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer, warps 2-5
+//   epilogue.  One output tile per CTA; optional split-K over blockIdx.z.
+// * gemm_simt_kernel (fp32 parity mode, "single precision"): plain FFMA, 128 x 64 tile,
+//   one output row per thread, fixed ascending-k accumulation -- same epilogue interface.
+#pragma once
+#include "ptx.cuh"
+
+namespace mlstm {
+
+template <int BN>
+struct TcCfg {
+  static constexpr int BM = 128, BK = 64;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int BN, class Epi>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                   int N, int K, int az, int bz, int kb_per_split, Epi epi) {
+  using C = TcCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* accf = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * C::BM, n0 = blockIdx.x * BN;
+  const int total_kb = (K + C::BK - 1) / C::BK;
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int nkb = max(0, min(kb_per_split, total_kb - kb0));
+
+  if (threadIdx.x == 0) {
+#pragma unroll 1
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::mbar_init(accf, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(tmem_slot, BN);
+    ptx::tmem_relinquish();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && nkb > 0) {
+      const uint64_t pol = ptx::policy_evict_last();
+#pragma unroll 1
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % C::STAGES;
+        const uint32_t ph = (i / C::STAGES) & 1;
+        ptx::mbar_wait(&empty[s], ph ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+        const int kc = (kb0 + i) * C::BK;
+        ptx::tma_load_3d(sA + s * C::A_BYTES, &tmA, &full[s], kc, m0, az, pol);
+        ptx::tma_load_3d(sB + s * C::B_BYTES, &tmB, &full[s], kc, n0, bz, pol);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nkb > 0) {
+      constexpr uint32_t idesc = ptx::idesc_f16_f32(C::BM, BN);
+#pragma unroll 1
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % C::STAGES;
+        const uint32_t ph = (i / C::STAGES) & 1;
+        ptx::mbar_wait(&full[s], ph);
+        ptx::tc_fence_after();
+        const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
+        const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
+#pragma unroll
+        for (int k = 0; k < C::BK / 16; ++k)
+          ptx::mma_f16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
+        ptx::mma_commit(&empty[s]);
+      }
+      ptx::mma_commit(accf);
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = m0 + q * 32 + lane;
+    if (nkb > 0) {
+      ptx::mbar_wait(accf, 0);
+      ptx::tc_fence_after();
+    }
+#pragma unroll 1
+    for (int c = 0; c < BN / 64; ++c) {
+      float v[64];
+      if (nkb > 0) {
+        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 64;
+        ptx::tmem_ld16(ta, v);
+        ptx::tmem_ld16(ta + 16, v + 16);
+        ptx::tmem_ld16(ta + 32, v + 32);
+        ptx::tmem_ld16(ta + 48, v + 48);
+        ptx::tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) v[i] = 0.f;
+      }
+      const int col0 = n0 + c * 64;
+      if (row < M && col0 < N) epi(row, col0, v);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, BN);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ float ld_as_float(const T* p) {
+  return static_cast<float>(*p);
+}
+template <>
+__device__ __forceinline__ float ld_as_float<__half>(const __half* p) {
+  return __half2float(*p);
+}
+
+// SIMT engine: 128 x 64 output tile, 128 threads, thread t owns row m0 + t.  K is consumed in
+// chunks of 32 staged through shared memory; k runs in ascending order inside each split.
+template <typename T, class Epi>
+__global__ void __launch_bounds__(128)
+    gemm_simt_kernel(const T* __restrict__ A, long lda, const T* __restrict__ B, long ldb, int M, int N, int K,
+                     int k_per_split, Epi epi) {
+  __shared__ float As[32][129];
+  __shared__ __align__(16) float Bs[32][64];
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.y * 128, n0 = blockIdx.x * 64;
+  const int kbeg = blockIdx.z * k_per_split;
+  const int kend = min(K, kbeg + k_per_split);
+  float acc[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+#pragma unroll 1
+  for (int kk = kbeg; kk < kend; kk += 32) {
+#pragma unroll 4
+    for (int i = tid; i < 128 * 32; i += 128) {
+      const int r = i >> 5, k = i & 31, gr = m0 + r, gk = kk + k;
+      As[k][r] = (gr < M && gk < kend) ? ld_as_float(A + (long)gr * lda + gk) : 0.f;
+    }
+#pragma unroll 4
+    for (int i = tid; i < 64 * 32; i += 128) {
+      const int n = i >> 5, k = i & 31, gn = n0 + n, gk = kk + k;
+      Bs[k][n] = (gn < N && gk < kend) ? ld_as_float(B + (long)gn * ldb + gk) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int k = 0; k < 32; ++k) {
+      const float a = As[k][tid];
+      const float4* b4 = reinterpret_cast<const float4*>(&Bs[k][0]);
+#pragma unroll
+      for (int n = 0; n < 16; ++n) {
+        const float4 bb = b4[n];
+        acc[4 * n + 0] = fmaf(a, bb.x, acc[4 * n + 0]);
+        acc[4 * n + 1] = fmaf(a, bb.y, acc[4 * n + 1]);
+        acc[4 * n + 2] = fmaf(a, bb.z, acc[4 * n + 2]);
+        acc[4 * n + 3] = fmaf(a, bb.w, acc[4 * n + 3]);
+      }
+    }
+    __syncthreads();
+  }
+  const int row = m0 + tid;
+  if (row < M && n0 < N) epi(row, n0, acc);
+}
+
+}  // namespace mlstm

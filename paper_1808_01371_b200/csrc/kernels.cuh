@@ -1,0 +1,436 @@
+// kernels.cuh -- the non-GEMM kernels of the step.
+//   (d)  ce_kernel / ce_reduce_kernel: fused softmax cross-entropy + BPC partials + dY over the
+//        256-byte vocabulary, warp-shuffle reductions, fp32 logits, fp32/fp64 sums.
+//   (e)  overflow_kernel + adam_kernel + scaler_kernel: overflow check on the reduced fp16
+//        gradients, skip-and-halve / grow loss scaling, unscale + Adam on fp32
+//        masters with the linear LR decay, fp16 working-copy cast.
+//   plus init (Q12), state carry / reset, one-hot, TBTT gate backward of the last
+//   step, weight-gradient finalisation and the per-byte segmented-sum reductions (dE, dW_x, db).
+#pragma once
+#include "epilogues.cuh"
+
+namespace mlstm {
+
+// ------------------------------------------------------------------ init (reading Q12)
+__device__ __forceinline__ uint64_t splitmix64_at(uint64_t seed, uint64_t q) {
+  uint64_t z = seed + (q + 1ull) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void init_params_kernel(float* master, ParamOffsets po, int h, int e, uint64_t seed) {
+  for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < po.P; q += (long)gridDim.x * blockDim.x) {
+    int cols = 0;  // fan-in of the matrix holding q; 0 for biases
+    if (q < po.Wmx) cols = e;
+    else if (q < po.Wmh) cols = e;
+    else if (q < po.Wx) cols = h;
+    else if (q < po.Wh) cols = e;
+    else if (q < po.b) cols = h;
+    else if (q < po.Wdec) cols = 0;
+    else if (q < po.bdec) cols = h;
+    float w = 0.f;
+    if (cols) {
+      const double u = (double)(splitmix64_at(seed, (uint64_t)q) >> 11) * 0x1.0p-53;
+      const double s = 1.0 / sqrt((double)cols);
+      w = __double2float_rn(s * (2.0 * u - 1.0));
+    }
+    master[q] = w;
+  }
+}
+
+// Write one master value into the fp16 (S) working copies the GEMMs read (gate-interleaved rows
+// for W_x and W_h, see net.cuh).  Biases have no working copy: epilogues read the fp32 masters.
+template <typename S>
+__device__ __forceinline__ void store_working(const Net<S>& n, long q, float val) {
+  const ParamOffsets& po = n.po;
+  const int h = n.h, e = n.e;
+  if (q < po.Wmx) {
+    n.E_w[q] = to_s<S>(val);
+  } else if (q < po.Wmh) {
+    n.Wcat_w[q - po.Wmx] = to_s<S>(val);
+  } else if (q < po.Wx) {
+    n.Wmh_w[q - po.Wmh] = to_s<S>(val);
+  } else if (q < po.Wh) {
+    const long r = (q - po.Wx) / e, c = (q - po.Wx) % e;
+    n.Wcat_w[((long)h + int_row((int)(r / h), (int)(r % h))) * e + c] = to_s<S>(val);
+  } else if (q < po.b) {
+    const long r = (q - po.Wh) / h, c = (q - po.Wh) % h;
+    n.Wh_w[(long)int_row((int)(r / h), (int)(r % h)) * h + c] = to_s<S>(val);
+  } else if (q >= po.Wdec && q < po.bdec) {
+    n.Wdec_w[q - po.Wdec] = to_s<S>(val);
+  }
+}
+
+template <typename S>
+__global__ void cast_working_kernel(Net<S> n) {
+  for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n.po.P; q += (long)gridDim.x * blockDim.x)
+    store_working(n, q, n.master[q]);
+}
+
+// dst[c][r] = src[r][c], src [R x C] row-major.
+template <typename S>
+__global__ void transpose_kernel(const S* __restrict__ src, S* __restrict__ dst, int R, int C) {
+  __shared__ S tile[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    if (r < R && c < C) tile[i][threadIdx.x] = src[(long)r * C + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (r < R && c < C) dst[(long)c * R + r] = tile[threadIdx.x][i];
+  }
+}
+
+// ------------------------------------------------------------------ state carry
+template <typename S>
+__global__ void state_in_kernel(Net<S> n, int slot) {
+  const long BH = (long)n.B * n.h;
+  if (blockIdx.x == 0 && threadIdx.x == 0) n.st->overflow = 0;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < BH; i += (long)gridDim.x * blockDim.x) {
+    const int b = (int)(i / n.h), j = (int)(i % n.h);
+    const bool rst = n.reset[b] != 0;
+    const S hv = rst ? to_s<S>(0.f) : n.hstate[slot * BH + i];
+    const float cv = rst ? 0.f : n.cstate[slot * BH + i];
+    n.Hrm[i] = hv;
+    n.HT[(long)j * n.ldH + b] = hv;
+    n.Crm[i] = cv;
+  }
+}
+
+template <typename S>
+__global__ void state_out_kernel(Net<S> n, int slot) {
+  const long BH = (long)n.B * n.h;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < BH; i += (long)gridDim.x * blockDim.x) {
+    n.hstate[slot * BH + i] = n.Hrm[(long)n.T * BH + i];
+    n.cstate[slot * BH + i] = n.Crm[(long)n.T * BH + i];
+  }
+}
+
+// One-hot of the input bytes, transposed: OHT[v][t*Bp+b] = [bytes[b][t] == v] (exact in fp16).
+template <typename S>
+__global__ void onehot_kernel(Net<S> n) {
+  const long TB = (long)n.T * n.B;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < TB; i += (long)gridDim.x * blockDim.x) {
+    const int t = (int)(i / n.B), b = (int)(i % n.B);
+    const int v0 = n.byte_at(b, t);
+    const long kc = n.kcol(t, b);
+    for (int v = 0; v < 256; ++v) n.OHT[(long)v * n.ldK + kc] = to_s<S>(v == v0 ? 1.f : 0.f);
+  }
+}
+
+// ------------------------------------------------------------------ (d) softmax cross-entropy
+// Block = 8 warps = 32 logit rows (row r = t*B + b); one warp per row, 8 logits per lane.
+// loss_r = logsumexp(y_r) - y_r[target] (max-subtracted, fp32);  dY = (softmax - onehot) *
+// alpha / (B_g T) (Q7).  Emits dY row-major and transposed (for dW_dec), per-block loss
+// and column sums (for db_dec), all in fixed order (deterministic).
+template <typename S>
+__global__ void __launch_bounds__(256) ce_kernel(Net<S> n, int Be, float inv_denom, int with_grad) {
+  __shared__ float tile[32][257];
+  __shared__ float rl[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long R = (long)n.T * n.B;
+  const long r0 = (long)blockIdx.x * 32;
+  const float coef = with_grad ? n.st->alpha * inv_denom : 0.f;
+#pragma unroll 1
+  for (int i = 0; i < 4; ++i) {
+    const int lr = warp * 4 + i;
+    const long r = r0 + lr;
+    const int t = r < R ? (int)(r / n.B) : 0;
+    const int b = r < R ? (int)(r % n.B) : 0;
+    const bool valid = r < R && b < Be;
+    float y[8];
+    if (valid) {
+      const float4 a = reinterpret_cast<const float4*>(n.Y + r * 256)[lane];
+      const float4 c = reinterpret_cast<const float4*>(n.Y + r * 256 + 128)[lane];
+      y[0] = a.x; y[1] = a.y; y[2] = a.z; y[3] = a.w;
+      y[4] = c.x; y[5] = c.y; y[6] = c.z; y[7] = c.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) y[k] = 0.f;
+    }
+    float mx = y[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) mx = fmaxf(mx, y[k]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float ex[8], se = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      ex[k] = expf(y[k] - mx);
+      se += ex[k];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const int tgt = valid ? n.byte_at(b, t + 1) : 0;
+    const int within = tgt & 127, owner = within >> 2, comp = (tgt >> 7) * 4 + (within & 3);
+    float sel = y[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) sel = (k == comp) ? y[k] : sel;
+    const float yt = __shfl_sync(0xffffffffu, sel, owner);
+    const float loss = valid ? (mx + logf(se)) - yt : 0.f;
+    if (lane == 0) {
+      rl[lr] = loss;
+      if (r < R) n.lossrow[r] = loss;
+    }
+    if (with_grad) {
+      const float inv = 1.f / se;
+      float g[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int col = (k < 4) ? lane * 4 + k : 128 + lane * 4 + (k - 4);
+        float p = ex[k] * inv;
+        if (col == tgt) p -= 1.f;
+        g[k] = valid ? p * coef : 0.f;
+        tile[lr][col] = g[k];
+      }
+      if (r < R) {
+        S* drow = n.dY + r * 256;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          drow[lane * 4 + k] = to_s<S>(g[k]);
+          drow[128 + lane * 4 + k] = to_s<S>(g[4 + k]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < 32; ++i) s += (double)rl[i];
+    n.loss_part[blockIdx.x] = s;
+  }
+  if (with_grad) {
+    {
+      const int v = threadIdx.x;
+      float s = 0.f;
+      for (int i = 0; i < 32; ++i) s += tile[i][v];
+      n.colsum_part[(long)blockIdx.x * 256 + v] = s;
+    }
+    const long r = r0 + lane;
+    if (r < R) {
+      const long kc = n.kcol((int)(r / n.B), (int)(r % n.B));
+#pragma unroll 4
+      for (int vv = 0; vv < 32; ++vv) {
+        const int v = warp * 32 + vv;
+        n.dYT[(long)v * n.ldK + kc] = to_s<S>(tile[lane][v]);
+      }
+    }
+  }
+}
+
+// Final fixed-order reductions of the CE partials: local loss sum -> st->loss_sum; db_dec.
+template <typename S>
+__global__ void __launch_bounds__(256) ce_reduce_kernel(Net<S> n, int nblk, int with_grad) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += 256) s += n.loss_part[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) n.st->loss_sum = red[0];
+  if (with_grad) {
+    const int v = threadIdx.x;
+    float cs = 0.f;
+    for (int i = 0; i < nblk; ++i) cs += n.colsum_part[(long)i * 256 + v];
+    n.arena[n.po.bdec + v] = to_s<S>(cs);
+  }
+}
+
+// ------------------------------------------------------------------ (c-1) TBTT start of BPTT
+// Gate backward of the last step s = T-1: dH = dH_dec only, dC carry = 0 (memset before).
+template <typename S>
+__global__ void gate_bwd_last_kernel(Net<S> n) {
+  const int nblk = n.h / 16;
+  const long total = (long)n.B * nblk;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int b = (int)(i / nblk), j0 = (int)(i % nblk) * 16;
+    const int s = n.T - 1;
+    float dh[16];
+    ld16(n.dHdec + ((long)s * n.B + b) * n.h + j0, dh);
+    gate_bwd16(n, s, b, j0, dh);
+  }
+}
+
+// ------------------------------------------------------------------ (c-2) weight gradients
+// Store modes: 0 = identity into the arena at `off`; 1 = W_h rows internal -> canonical;
+// 2 = per-byte segmented sums into Scan[256][5h] with canonical columns.
+__device__ __forceinline__ long wgrad_col_canon(int mode, int c, int h) {
+  return (mode == 2 && c >= h) ? (long)h + canon_of_int(c - h, h) : c;
+}
+
+template <typename S>
+struct EpiWgrad {
+  Net<S> n;
+  long off;
+  int mode;
+  int N;
+  __device__ __forceinline__ void operator()(int row, int col0, float (&v)[64]) const {
+    if (mode == 2) {
+      float* dst = n.Scan + (long)row * 5 * n.h;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) dst[wgrad_col_canon(2, col0 + i, n.h)] = v[i];
+      return;
+    }
+    const long r = (mode == 1) ? canon_of_int(row, n.h) : row;
+    S* dst = n.arena + off + r * N + col0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) st16(dst + 16 * q, v + 16 * q);
+  }
+};
+
+template <typename S>
+__global__ void wgrad_finalize_kernel(Net<S> n, const float* __restrict__ part, int splits, int M, int N, long off,
+                                      int mode) {
+  const long MN = (long)M * N;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < MN; i += (long)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += part[z * MN + i];
+    const int row = (int)(i / N), col = (int)(i % N);
+    if (mode == 2) {
+      n.Scan[(long)row * 5 * n.h + wgrad_col_canon(2, col, n.h)] = s;
+    } else {
+      const long r = (mode == 1) ? canon_of_int(row, n.h) : row;
+      n.arena[off + r * N + col] = to_s<S>(s);
+    }
+  }
+}
+
+// dW_mx = S_mx^T E, dW_x = S_x^T E  (X = E[bytes] so dZ^T X = sum_v S[v]^T E[v]); fp32 accumulate.
+template <typename S>
+__global__ void dwcat_kernel(Net<S> n) {
+  const int h = n.h, e = n.e;
+  const int r = blockIdx.x * blockDim.y + threadIdx.y;  // canonical row of [W_mx; W_x], < 5h
+  if (r >= 5 * h) return;
+  for (int c = threadIdx.x; c < e; c += blockDim.x) {
+    float s = 0.f;
+    for (int v = 0; v < 256; ++v) s += n.Scan[(long)v * 5 * h + r] * to_f(n.E_w[(long)v * e + c]);
+    const long dst = (r < h) ? n.po.Wmx + (long)r * e + c : n.po.Wx + (long)(r - h) * e + c;
+    n.arena[dst] = to_s<S>(s);
+  }
+}
+
+// dE[v] = sum_r S[v][r] [W_mx; W_x][r]  (the embedding gradient, segmented by byte), and
+// db = sum_v S_x[v].
+template <typename S>
+__global__ void __launch_bounds__(256) de_kernel(Net<S> n) {
+  __shared__ float red[4][64];
+  const int h = n.h, e = n.e, v = blockIdx.x;
+  const int grp = threadIdx.x >> 6, cl = threadIdx.x & 63;
+  const int R = 5 * h, per = (R + 3) / 4;
+  for (int c0 = 0; c0 < e; c0 += 64) {
+    const int c = c0 + cl;
+    float s = 0.f;
+    if (c < e) {
+      const int rb = grp * per, re = min(R, rb + per);
+      for (int r = rb; r < re; ++r) {
+        const long wrow = (r < h) ? r : (long)h + int_row((r - h) / h, (r - h) % h);
+        s += n.Scan[(long)v * R + r] * to_f(n.Wcat_w[wrow * e + c]);
+      }
+    }
+    red[grp][cl] = s;
+    __syncthreads();
+    if (grp == 0 && c < e) n.arena[n.po.E + (long)v * e + c] = to_s<S>(((red[0][cl] + red[1][cl]) + red[2][cl]) + red[3][cl]);
+    __syncthreads();
+  }
+}
+
+template <typename S>
+__global__ void db_kernel(Net<S> n) {
+  const int h = n.h;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < 4 * h; r += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int v = 0; v < 256; ++v) s += n.Scan[(long)v * 5 * h + h + r];
+    n.arena[n.po.b + r] = to_s<S>(s);
+  }
+}
+
+// ------------------------------------------------------------------ (e) optimiser
+__device__ __forceinline__ bool nonfinite_bits(__half x) {
+  return (__half_as_ushort(x) & 0x7C00u) == 0x7C00u;
+}
+__device__ __forceinline__ bool nonfinite_bits(float x) {
+  return (__float_as_uint(x) & 0x7F800000u) == 0x7F800000u;
+}
+
+// "checking for an overflow in the weight gradients": any inf/NaN in the buffer.
+template <typename S>
+__global__ void overflow_kernel(const S* __restrict__ buf, long count, int32_t* flag) {
+  bool bad = false;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x)
+    bad |= nonfinite_bits(buf[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 1;
+}
+
+// Unscale + Adam on fp32 masters + fp16 working-copy cast; a no-op when the step overflowed.
+template <typename S>
+__global__ void adam_kernel(Net<S> n, float* __restrict__ m, float* __restrict__ v, float beta1, float beta2,
+                            float eps, double lr0, long decay) {
+  const DevState* st = n.st;
+  if (st->overflow) return;
+  const float inv_alpha = 1.f / st->alpha;  // alpha is a power of two: exact
+  const long tau = st->tau + 1;
+  const double lr = lr0 * fmax(0.0, 1.0 - (double)st->it / (double)decay);
+  const float bc1 = (float)(1.0 - pow((double)beta1, (double)tau));
+  const float bc2 = (float)(1.0 - pow((double)beta2, (double)tau));
+  const float lrf = (float)lr;
+  for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n.po.P; q += (long)gridDim.x * blockDim.x) {
+    const float g = to_f(n.arena[q]) * inv_alpha;
+    const float mm = beta1 * m[q] + (1.f - beta1) * g;
+    const float vv = beta2 * v[q] + (1.f - beta2) * g * g;
+    const float th = n.master[q] - lrf * (mm / bc1) / (sqrtf(vv / bc2) + eps);
+    m[q] = mm;
+    v[q] = vv;
+    n.master[q] = th;
+    store_working(n, q, th);
+  }
+}
+
+// Loss-scale state machine + LR clock / Adam count (Q10).  One thread.
+__global__ void scaler_kernel(DevState* st, float smin, float smax, int interval, double lr0, long decay) {
+  const int ovf = st->overflow;
+  st->alpha_used = st->alpha;
+  st->lr_used = lr0 * fmax(0.0, 1.0 - (double)st->it / (double)decay);
+  st->skipped = ovf;
+  if (ovf) {
+    st->alpha = fmaxf(st->alpha * 0.5f, smin);
+    st->clean = 0;
+  } else {
+    st->tau += 1;
+    st->clean += 1;
+    if (st->clean >= interval) {
+      st->alpha = fminf(st->alpha * 2.f, smax);
+      st->clean = 0;
+    }
+  }
+  st->it += 1;
+}
+
+// Debug: X = E_w[bytes] as the kernels index it ([T][B][e], fp32).
+template <typename S>
+__global__ void gather_x_kernel(Net<S> n, float* out) {
+  const long total = (long)n.T * n.B * n.e;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const long tb = i / n.e;
+    const int c = (int)(i % n.e), t = (int)(tb / n.B), b = (int)(tb % n.B);
+    out[i] = to_f(n.E_w[(long)n.byte_at(b, t) * n.e + c]);
+  }
+}
+
+template <typename S>
+__global__ void to_float_kernel(const S* __restrict__ src, float* __restrict__ dst, long count) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x)
+    dst[i] = to_f(src[i]);
+}
+template <typename S>
+__global__ void from_float_kernel(const float* __restrict__ src, S* __restrict__ dst, long count) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x)
+    dst[i] = to_s<S>(src[i]);
+}
+
+}  // namespace mlstm

@@ -1,0 +1,1048 @@
+// mlstm.cu -- host orchestrator and C ABI of libmlstm.so (include/mlstm.h).
+//
+// One context per rank.  A train step is enqueued on the caller's stream as two CUDA graphs
+// (recorded on first use): A = forward + CE + BPTT + weight gradients, B = overflow check +
+// scaler + Adam + cast + state carry, with the NCCL fp16 SUM allreduce of the gradient arena
+// between them when world > 1.  See DESIGN.md for the data layout and kernel list.
+#include <cudaTypedefs.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/mlstm.h"
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+using namespace mlstm;
+
+namespace {
+
+thread_local std::string g_err;
+
+enum Phase { PH_PREP, PH_TAB, PH_FWD, PH_DEC, PH_CE, PH_DHDEC, PH_BWD, PH_WGRAD, PH_ALLREDUCE, PH_OPT, NPH };
+const char* kPhaseNames[NPH] = {"prep", "tab", "fwd_rec", "decoder", "ce", "dhdec",
+                                "bwd_rec", "wgrad", "allreduce", "optimizer"};
+
+struct Opd {  // K-major operand view: [zdim][rows][K], element strides ld (row) and zstride
+  const void* ptr;
+  long rows, K, ld, zdim, zstride;
+};
+
+struct Plan {
+  int bn, splits;
+};
+
+long rup(long x, long m) { return (x + m - 1) / m * m; }
+
+}  // namespace
+
+struct mlstm_ctx {
+  mlstm_config cfg{};
+  int rank = 0, world = 1;
+  cudaStream_t stream = nullptr;   // caller's stream: every launch and graph launch goes here
+  cudaStream_t cap = nullptr;      // private stream graphs are recorded on (the caller's may be
+                                   // the legacy default stream, which cannot be captured)
+  bool mixed = true, tc = true;
+  int h = 0, e = 0, B = 0, T = 0, Bp = 0;
+  long ldK = 0, ldH = 0, P = 0, Kt = 0;
+  ParamOffsets po{};
+  uint8_t* ws = nullptr;
+  size_t ws_bytes = 0;
+  // buffers that are not in Net
+  float *adam_m = nullptr, *adam_v = nullptr;
+  uint8_t *bytes = nullptr, *reset = nullptr;
+  int32_t* scratch_flag = nullptr;
+  DevState* st = nullptr;
+  DevState* st_host = nullptr;  // pinned
+  int nblk_ce = 0;
+  long part_elems = 0;
+  Net<__half> nh{};
+  Net<float> nf{};
+  ncclComm_t comm = nullptr;
+  cudaGraphExec_t gA = nullptr, gB = nullptr;
+  std::map<std::tuple<const void*, long, long, long, long, long, int>, CUtensorMap> maps;
+  mlstm_status failed = MLSTM_OK;
+  bool have_last = false;
+  DevState last{};
+  int nonfinite_run = 0;
+  // profiling
+  bool profile = false;
+  cudaEvent_t ev[NPH + 1] = {};
+  double phase_ms[NPH] = {};
+  int32_t phase_launches[NPH] = {};
+  int cur_phase = 0;
+  int launches = 0;
+  bool counting = false;
+};
+
+namespace {
+
+mlstm_status fail(mlstm_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_OR_FAIL(ctx, x)                                                                   \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) {                                                                   \
+      if (ctx) (ctx)->failed = MLSTM_ECUDA;                                                    \
+      return fail(MLSTM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));               \
+    }                                                                                          \
+  } while (0)
+
+#define NCCL_OR_FAIL(ctx, x)                                                                   \
+  do {                                                                                         \
+    ncclResult_t r_ = (x);                                                                     \
+    if (r_ != ncclSuccess) {                                                                   \
+      if (ctx) (ctx)->failed = MLSTM_ENCCL;                                                    \
+      return fail(MLSTM_ENCCL, std::string(#x) + ": " + ncclGetErrorString(r_));               \
+    }                                                                                          \
+  } while (0)
+
+// ------------------------------------------------------------------ workspace layout
+struct Carver {
+  uint8_t* base;
+  size_t off = 0;
+  template <typename X>
+  X* take(long count) {
+    off = rup((long)off, 256);
+    X* p = base ? reinterpret_cast<X*>(base + off) : nullptr;
+    off += (size_t)count * sizeof(X);
+    return p;
+  }
+};
+
+int grid_for(long n, int threads = 256, int cap = 148 * 16) {
+  long g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+// Tile-N and split-K choice shared by the workspace layout and the launches.
+Plan plan_gemm(bool tc, long M, long N, long K, bool allow_split) {
+  Plan p{64, 1};
+  const long mt = (M + 127) / 128;
+  if (tc) {
+    for (int bn : {256, 128, 64}) {
+      if (mt * ((N + bn - 1) / bn) >= 120 || bn == 64) {
+        p.bn = bn;
+        break;
+      }
+    }
+  }
+  if (allow_split) {
+    const long tiles = mt * ((N + p.bn - 1) / p.bn);
+    const long kb = (K + 63) / 64;
+    while (tiles * p.splits < 148 && kb / (p.splits * 2) >= 4) p.splits *= 2;
+  }
+  return p;
+}
+
+template <typename S>
+void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
+  const int h = c->h, e = c->e, B = c->B, T = c->T;
+  const long P = c->P;
+  n.h = h; n.e = e; n.B = B; n.T = T; n.Bp = c->Bp;
+  n.ldK = c->ldK; n.ldH = c->ldH; n.po = c->po;
+  n.master = cv.take<float>(P);
+  c->adam_m = cv.take<float>(P);
+  c->adam_v = cv.take<float>(P);
+  n.arena = cv.take<S>(P);
+  n.E_w = cv.take<S>(256L * e);
+  n.Wcat_w = cv.take<S>(5L * h * e);
+  n.Wmh_w = cv.take<S>((long)h * h);
+  n.Wh_w = cv.take<S>(4L * h * h);
+  n.Wdec_w = cv.take<S>(256L * h);
+  n.WmhT = cv.take<S>((long)h * h);
+  n.WhT = cv.take<S>(4L * h * h);
+  n.WdecT = cv.take<S>(256L * h);
+  c->bytes = cv.take<uint8_t>((long)B * (T + 1));
+  c->reset = cv.take<uint8_t>(B);
+  n.bytes = c->bytes;
+  n.reset = c->reset;
+  n.tab = cv.take<float>(256L * 5 * h);
+  n.Hrm = cv.take<S>((long)(T + 1) * B * h);
+  n.HT = cv.take<S>((long)h * c->ldH);
+  n.Crm = cv.take<float>((long)(T + 1) * B * h);
+  n.Mscr = cv.take<S>((long)B * h);
+  n.MT = cv.take<S>((long)h * c->ldK);
+  n.Astash = cv.take<S>((long)T * B * h);
+  n.Gates = cv.take<S>((long)T * B * 4 * h);
+  n.Y = cv.take<float>((long)T * B * 256);
+  n.lossrow = cv.take<float>((long)T * B);
+  n.dY = cv.take<S>((long)T * B * 256);
+  n.dYT = cv.take<S>(256L * c->ldK);
+  n.OHT = cv.take<S>(256L * c->ldK);
+  n.dHdec = cv.take<float>((long)T * B * h);
+  n.dZscr = cv.take<S>((long)B * 4 * h);
+  n.dAscr = cv.take<S>((long)B * h);
+  n.dC = cv.take<float>((long)B * h);
+  n.dGT = cv.take<S>(5L * h * c->ldK);
+  n.dAT = cv.take<S>((long)h * c->ldK);
+  // split-K partial buffer: the largest split GEMM among the weight gradients
+  long part = 64;
+  const long K = c->Kt;
+  const long shapes[4][2] = {{4L * h, h}, {h, h}, {256, h}, {256, 5L * h}};
+  for (auto& s : shapes) {
+    Plan p = plan_gemm(c->tc, s[0], s[1], K, true);
+    if (p.splits > 1) part = std::max(part, (long)p.splits * s[0] * s[1]);
+  }
+  c->part_elems = part;
+  n.part = cv.take<float>(part);
+  n.Scan = cv.take<float>(256L * 5 * h);
+  n.hstate = cv.take<S>(2L * B * h);
+  n.cstate = cv.take<float>(2L * B * h);
+  c->nblk_ce = (int)(((long)T * B + 31) / 32);
+  n.loss_part = cv.take<double>(c->nblk_ce);
+  n.colsum_part = cv.take<float>((long)c->nblk_ce * 256);
+  n.st = cv.take<DevState>(1);
+  c->st = n.st;
+  c->scratch_flag = cv.take<int32_t>(4);
+}
+
+mlstm_status validate(const mlstm_config* cfg) {
+  if (!cfg) return fail(MLSTM_EINVAL, "null config");
+  if (cfg->hidden <= 0 || cfg->hidden % 64) return fail(MLSTM_EINVAL, "hidden must be a positive multiple of 64");
+  if (cfg->embed <= 0 || cfg->embed % 64) return fail(MLSTM_EINVAL, "embed must be a positive multiple of 64");
+  if (cfg->vocab != 256) return fail(MLSTM_EINVAL, "vocab must be 256 (byte level)");
+  if (cfg->seq_len <= 0 || cfg->batch <= 0) return fail(MLSTM_EINVAL, "seq_len and batch must be positive");
+  if (cfg->micro_batch != 0 && cfg->micro_batch != cfg->batch)
+    return fail(MLSTM_EINVAL, "micro_batch must be 0 in this version");
+  if (cfg->weight_norm != 0) return fail(MLSTM_EINVAL, "weight_norm must be 0 in this version (DESIGN Q4)");
+  if (cfg->precision != MLSTM_FP32 && cfg->precision != MLSTM_MIXED) return fail(MLSTM_EINVAL, "bad precision");
+  if (!(cfg->decay_iters > 0) || !(cfg->lr0 >= 0)) return fail(MLSTM_EINVAL, "bad LR schedule");
+  if (!(cfg->scale_min > 0) || !(cfg->scale_max >= cfg->scale_min) || !(cfg->scale_init >= cfg->scale_min) ||
+      !(cfg->scale_init <= cfg->scale_max) || cfg->scale_growth_interval <= 0)
+    return fail(MLSTM_EINVAL, "bad loss-scale settings");
+  return MLSTM_OK;
+}
+
+void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
+  c->cfg = *cfg;
+  c->h = cfg->hidden;
+  c->e = cfg->embed;
+  c->B = cfg->batch;
+  c->T = cfg->seq_len;
+  c->Bp = (int)rup(c->B, 8);
+  c->Kt = (long)c->T * c->Bp;
+  c->ldK = rup(c->Kt, 64);
+  c->ldH = rup((long)(c->T + 1) * c->Bp, 64);
+  c->po.set(c->h, c->e);
+  c->P = c->po.P;
+  c->mixed = cfg->precision == MLSTM_MIXED;
+  const char* dbg = getenv("MLSTM_DEBUG_SIMT_GEMM");  // test instrument: mixed mode on the SIMT engine
+  c->tc = c->mixed && !(dbg && dbg[0] == '1');
+}
+
+size_t layout_bytes(mlstm_ctx* c) {
+  Carver cv{nullptr};
+  if (c->mixed) {
+    Net<__half> n{};
+    carve(c, cv, n);
+  } else {
+    Net<float> n{};
+    carve(c, cv, n);
+  }
+  return cv.off + 256;
+}
+
+// ------------------------------------------------------------------ launches
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+bool get_encoder() {
+  if (g_encode) return true;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn)
+    return false;
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return true;
+}
+
+const CUtensorMap* get_map(mlstm_ctx* c, const Opd& o, int box_rows) {
+  auto key = std::make_tuple(o.ptr, o.rows, o.K, o.ld, o.zdim, o.zstride, box_rows);
+  auto it = c->maps.find(key);
+  if (it != c->maps.end()) return &it->second;
+  CUtensorMap m;
+  cuuint64_t dims[3] = {(cuuint64_t)o.K, (cuuint64_t)o.rows, (cuuint64_t)o.zdim};
+  cuuint64_t strides[2] = {(cuuint64_t)o.ld * 2, (cuuint64_t)o.zstride * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(o.ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d) rows=%ld K=%ld ld=%ld", (int)r, o.rows, o.K, o.ld);
+    g_err = buf;
+    return nullptr;
+  }
+  return &(c->maps[key] = m);
+}
+
+void count_launch(mlstm_ctx* c) {
+  if (c->counting) {
+    c->launches++;
+    c->phase_launches[c->cur_phase]++;
+  }
+}
+
+template <int BN, class Epi>
+cudaError_t launch_tc(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az, int bz,
+                      int splits, const Epi& epi) {
+  auto kern = gemm_tc_kernel<BN, Epi>;
+  const int smem = TcCfg<BN>::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int kb = (K + 63) / 64;
+  const int kbps = (kb + splits - 1) / splits;
+  dim3 grid((N + BN - 1) / BN, (M + 127) / 128, splits);
+  kern<<<grid, 192, smem, c->stream>>>(*ma, *mb, M, N, K, az, bz, kbps, epi);
+  count_launch(c);
+  return cudaGetLastError();
+}
+
+// D[M x N] = A[az] . B[bz]^T, fused epilogue.  `splits` > 1 only with a partial epilogue.
+template <typename S, class Epi>
+mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int M, int N, int K, Plan p,
+                  const Epi& epi) {
+  if constexpr (std::is_same<S, __half>::value) {
+    if (c->tc) {
+    const CUtensorMap* ma = get_map(c, A, 128);
+    const CUtensorMap* mb = get_map(c, B, p.bn);
+    if (!ma || !mb) {
+      c->failed = MLSTM_ECUDA;
+      return MLSTM_ECUDA;
+    }
+    cudaError_t e;
+    switch (p.bn) {
+      case 256: e = launch_tc<256>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
+      case 128: e = launch_tc<128>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
+      default: e = launch_tc<64>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
+    }
+    CUDA_OR_FAIL(c, e);
+    return MLSTM_OK;
+    }
+  }
+  const S* a = static_cast<const S*>(A.ptr) + (long)az * A.zstride;
+  const S* b = static_cast<const S*>(B.ptr) + (long)bz * B.zstride;
+  const int kps = (int)rup((K + p.splits - 1) / p.splits, 32);
+  dim3 grid((N + 63) / 64, (M + 127) / 128, p.splits);
+  gemm_simt_kernel<S, Epi><<<grid, 128, 0, c->stream>>>(a, A.ld, b, B.ld, M, N, K, kps, epi);
+  count_launch(c);
+  CUDA_OR_FAIL(c, cudaGetLastError());
+  return MLSTM_OK;
+}
+
+#define RET_IF(x)                         \
+  do {                                    \
+    mlstm_status s_ = (x);                \
+    if (s_ != MLSTM_OK) return s_;        \
+  } while (0)
+
+#define LAUNCH(c, ...)                        \
+  do {                                        \
+    __VA_ARGS__;                              \
+    count_launch(c);                          \
+    CUDA_OR_FAIL(c, cudaGetLastError());      \
+  } while (0)
+
+void phase(mlstm_ctx* c, int ph) {
+  c->cur_phase = ph;
+  // External: inside stream capture this becomes an event-record node that fires when the graph
+  // runs (a plain record would only be an intra-graph dependency marker).
+  if (c->profile) cudaEventRecordWithFlags(c->ev[ph], c->stream, cudaEventRecordExternal);
+}
+
+template <typename S>
+Net<S>& net(mlstm_ctx* c);
+template <>
+Net<__half>& net<__half>(mlstm_ctx* c) {
+  return c->nh;
+}
+template <>
+Net<float>& net<float>(mlstm_ctx* c) {
+  return c->nf;
+}
+
+// Recomputes the transposed working copies from the row-major ones.
+template <typename S>
+mlstm_status enqueue_transposes(mlstm_ctx* c) {
+  Net<S>& n = net<S>(c);
+  const int h = c->h;
+  dim3 blk(32, 8);
+  LAUNCH(c, (transpose_kernel<S><<<dim3((h + 31) / 32, (h + 31) / 32), blk, 0, c->stream>>>(n.Wmh_w, n.WmhT, h, h)));
+  LAUNCH(c, (transpose_kernel<S><<<dim3((h + 31) / 32, (4 * h + 31) / 32), blk, 0, c->stream>>>(n.Wh_w, n.WhT, 4 * h, h)));
+  LAUNCH(c, (transpose_kernel<S><<<dim3((h + 31) / 32, 256 / 32), blk, 0, c->stream>>>(n.Wdec_w, n.WdecT, 256, h)));
+  return MLSTM_OK;
+}
+
+template <typename S>
+mlstm_status enqueue_cast(mlstm_ctx* c) {
+  Net<S>& n = net<S>(c);
+  LAUNCH(c, (cast_working_kernel<S><<<grid_for(c->P), 256, 0, c->stream>>>(n)));
+  return enqueue_transposes<S>(c);
+}
+
+// Input projection table + forward recurrence over T steps (+ decoder logits).
+template <typename S>
+mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
+  Net<S>& n = net<S>(c);
+  const int h = c->h, e = c->e, B = c->B, T = c->T;
+  phase(c, PH_PREP);
+  LAUNCH(c, (state_in_kernel<S><<<grid_for((long)B * h), 256, 0, c->stream>>>(n, slot)));
+  phase(c, PH_TAB);
+  {
+    Opd A{n.E_w, 256, e, e, 1, 256L * e};
+    Opd Bo{n.Wcat_w, 5L * h, e, e, 1, 5L * h * e};
+    RET_IF(gemm<S>(c, A, 0, Bo, 0, 256, 5 * h, e, plan_gemm(c->tc, 256, 5 * h, e, false), EpiTab<S>{n}));
+  }
+  phase(c, PH_FWD);
+  const Opd Hprev{n.Hrm, B, h, h, T + 1, (long)B * h};
+  const Opd Wmh{n.Wmh_w, h, h, h, 1, (long)h * h};
+  const Opd Msc{n.Mscr, B, h, h, 1, (long)B * h};
+  const Opd Wh{n.Wh_w, 4L * h, h, h, 1, 4L * h * h};
+  const Plan p1 = plan_gemm(c->tc, B, h, h, false), p2 = plan_gemm(c->tc, B, 4 * h, h, false);
+  for (int t = 0; t < T; ++t) {
+    RET_IF(gemm<S>(c, Hprev, t, Wmh, 0, B, h, h, p1, EpiF1<S>{n, t}));
+    RET_IF(gemm<S>(c, Msc, 0, Wh, 0, B, 4 * h, h, p2, EpiF2<S>{n, t}));
+  }
+  phase(c, PH_DEC);
+  {
+    Opd A{n.Hrm + (long)B * h, (long)T * B, h, h, 1, (long)T * B * h};
+    Opd Bo{n.Wdec_w, 256, h, h, 1, 256L * h};
+    RET_IF(gemm<S>(c, A, 0, Bo, 0, T * B, 256, h, plan_gemm(c->tc, (long)T * B, 256, h, false), EpiY<S>{n}));
+  }
+  return MLSTM_OK;
+}
+
+template <typename S>
+mlstm_status enqueue_train_a(mlstm_ctx* c) {
+  Net<S>& n = net<S>(c);
+  const int h = c->h, B = c->B, T = c->T;
+  const long Kt = c->Kt;
+  RET_IF(enqueue_forward<S>(c, MLSTM_SLOT_TRAIN));
+  // the one-hot and the dC reset belong to the prep phase logically; they run here, off the
+  // forward's critical path
+  LAUNCH(c, (onehot_kernel<S><<<grid_for((long)T * B), 256, 0, c->stream>>>(n)));
+  CUDA_OR_FAIL(c, cudaMemsetAsync(n.dC, 0, sizeof(float) * (size_t)B * h, c->stream));
+  phase(c, PH_CE);
+  const double denom = (double)B * c->world * T;  // B_g * T (Q7)
+  LAUNCH(c, (ce_kernel<S><<<c->nblk_ce, 256, 0, c->stream>>>(n, B, (float)(1.0 / denom), 1)));
+  LAUNCH(c, (ce_reduce_kernel<S><<<1, 256, 0, c->stream>>>(n, c->nblk_ce, 1)));
+  phase(c, PH_DHDEC);
+  {
+    Opd A{n.dY, (long)T * B, 256, 256, 1, (long)T * B * 256};
+    Opd Bo{n.WdecT, h, 256, 256, 1, 256L * h};
+    RET_IF(gemm<S>(c, A, 0, Bo, 0, T * B, h, 256, plan_gemm(c->tc, (long)T * B, h, 256, false), EpiDHdec<S>{n}));
+  }
+  phase(c, PH_BWD);
+  LAUNCH(c, (gate_bwd_last_kernel<S><<<grid_for((long)B * h / 16), 256, 0, c->stream>>>(n)));
+  {
+    const Opd dZ{n.dZscr, B, 4L * h, 4L * h, 1, 4L * B * h};
+    const Opd WhT{n.WhT, h, 4L * h, 4L * h, 1, 4L * h * h};
+    const Opd dA{n.dAscr, B, h, h, 1, (long)B * h};
+    const Opd WmhT{n.WmhT, h, h, h, 1, (long)h * h};
+    const Plan p1 = plan_gemm(c->tc, B, h, 4 * h, false), p2 = plan_gemm(c->tc, B, h, h, false);
+    for (int t = T - 1; t >= 0; --t) {
+      RET_IF(gemm<S>(c, dZ, 0, WhT, 0, B, h, 4 * h, p1, EpiB1<S>{n, t}));
+      if (t > 0) RET_IF(gemm<S>(c, dA, 0, WmhT, 0, B, h, h, p2, EpiB2<S>{n, t - 1}));
+    }
+  }
+  phase(c, PH_WGRAD);
+  {
+    struct W {
+      Opd A, B;
+      long M, N, off;
+      int mode;
+    };
+    const W ws[4] = {
+        {{n.dGT + (long)h * c->ldK, 4L * h, Kt, c->ldK, 1, 4L * h * c->ldK}, {n.MT, h, Kt, c->ldK, 1, h * c->ldK},
+         4L * h, h, c->po.Wh, 1},                                                     // dW_h = dZ^T M
+        {{n.dAT, h, Kt, c->ldK, 1, h * c->ldK}, {n.HT, h, Kt, c->ldH, 1, h * c->ldH}, h, h, c->po.Wmh, 0},
+        // dW_mh = dA^T H_{t-1}
+        {{n.dYT, 256, Kt, c->ldK, 1, 256 * c->ldK}, {n.HT + c->Bp, h, Kt, c->ldH, 1, h * c->ldH}, 256, h,
+         c->po.Wdec, 0},                                                               // dW_dec = dY^T H
+        {{n.OHT, 256, Kt, c->ldK, 1, 256 * c->ldK}, {n.dGT, 5L * h, Kt, c->ldK, 1, 5L * h * c->ldK}, 256, 5L * h,
+         0, 2},                                                                        // S = onehot^T [dMX|dZ]
+    };
+    for (const W& w : ws) {
+      const Plan p = plan_gemm(c->tc, w.M, w.N, Kt, true);
+      if (p.splits == 1) {
+        RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kt, p, EpiWgrad<S>{n, w.off, w.mode, (int)w.N}));
+      } else {
+        RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kt, p, EpiPartial{n.part, w.N, w.M * w.N}));
+        LAUNCH(c, (wgrad_finalize_kernel<S><<<grid_for(w.M * w.N), 256, 0, c->stream>>>(n, n.part, p.splits, (int)w.M,
+                                                                                          (int)w.N, w.off, w.mode)));
+      }
+    }
+    LAUNCH(c, (dwcat_kernel<S><<<(5 * h + 3) / 4, dim3(64, 4), 0, c->stream>>>(n)));
+    LAUNCH(c, (de_kernel<S><<<256, 256, 0, c->stream>>>(n)));
+    LAUNCH(c, (db_kernel<S><<<grid_for(4L * h), 256, 0, c->stream>>>(n)));
+  }
+  return MLSTM_OK;
+}
+
+template <typename S>
+mlstm_status enqueue_train_b(mlstm_ctx* c) {
+  Net<S>& n = net<S>(c);
+  const mlstm_config& cf = c->cfg;
+  phase(c, PH_OPT);
+  LAUNCH(c, (overflow_kernel<S><<<grid_for(c->P), 256, 0, c->stream>>>(n.arena, c->P, &c->st->overflow)));
+  LAUNCH(c, (adam_kernel<S><<<grid_for(c->P), 256, 0, c->stream>>>(n, c->adam_m, c->adam_v, (float)cf.beta1,
+                                                                   (float)cf.beta2, (float)cf.eps, cf.lr0,
+                                                                   (long)cf.decay_iters)));
+  RET_IF(enqueue_transposes<S>(c));
+  LAUNCH(c, (scaler_kernel<<<1, 1, 0, c->stream>>>(c->st, cf.scale_min, cf.scale_max, cf.scale_growth_interval,
+                                                   cf.lr0, (long)cf.decay_iters)));
+  LAUNCH(c, (state_out_kernel<S><<<grid_for((long)c->B * c->h), 256, 0, c->stream>>>(n, MLSTM_SLOT_TRAIN)));
+  return MLSTM_OK;
+}
+
+template <typename S>
+mlstm_status record_graph(mlstm_ctx* c, mlstm_status (*fn)(mlstm_ctx*), cudaGraphExec_t* out) {
+  cudaGraph_t g = nullptr;
+  cudaStream_t user = c->stream;
+  c->stream = c->cap;
+  cudaError_t eb = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+  if (eb != cudaSuccess) {
+    c->stream = user;
+    CUDA_OR_FAIL(c, eb);
+  }
+  mlstm_status s = fn(c);
+  cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+  c->stream = user;
+  if (s != MLSTM_OK) {
+    if (g) cudaGraphDestroy(g);
+    return s;
+  }
+  CUDA_OR_FAIL(c, e);
+  CUDA_OR_FAIL(c, cudaGraphInstantiate(out, g, 0));
+  cudaGraphDestroy(g);
+  return MLSTM_OK;
+}
+
+template <typename S>
+mlstm_status build_graphs(mlstm_ctx* c) {
+  if (c->gA) cudaGraphExecDestroy(c->gA);
+  if (c->gB) cudaGraphExecDestroy(c->gB);
+  c->gA = c->gB = nullptr;
+  c->counting = true;
+  c->launches = 0;
+  memset(c->phase_launches, 0, sizeof c->phase_launches);
+  mlstm_status s = record_graph<S>(c, enqueue_train_a<S>, &c->gA);
+  if (s == MLSTM_OK) s = record_graph<S>(c, enqueue_train_b<S>, &c->gB);
+  c->counting = false;
+  return s;
+}
+
+template <typename S>
+mlstm_status run_train(mlstm_ctx* c) {
+  if (!c->gA) RET_IF(build_graphs<S>(c));
+  Net<S>& n = net<S>(c);
+  CUDA_OR_FAIL(c, cudaGraphLaunch(c->gA, c->stream));
+  if (c->world > 1) {
+    c->cur_phase = PH_ALLREDUCE;
+    if (c->profile) CUDA_OR_FAIL(c, cudaEventRecord(c->ev[PH_ALLREDUCE], c->stream));
+    NCCL_OR_FAIL(c, ncclAllReduce(n.arena, n.arena, (size_t)c->P, c->mixed ? ncclFloat16 : ncclFloat32, ncclSum,
+                                  c->comm, c->stream));
+    NCCL_OR_FAIL(c, ncclAllReduce(&c->st->loss_sum, &c->st->loss_sum, 1, ncclFloat64, ncclSum, c->comm, c->stream));
+  } else if (c->profile) {
+    CUDA_OR_FAIL(c, cudaEventRecord(c->ev[PH_ALLREDUCE], c->stream));
+  }
+  CUDA_OR_FAIL(c, cudaGraphLaunch(c->gB, c->stream));
+  if (c->profile) CUDA_OR_FAIL(c, cudaEventRecord(c->ev[NPH], c->stream));
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  return MLSTM_OK;
+}
+
+mlstm_status ctx_ok(mlstm_ctx* c) {
+  if (!c) return fail(MLSTM_EINVAL, "null context");
+  if (c->failed != MLSTM_OK) return fail(c->failed, "context failed earlier: " + g_err);
+  return MLSTM_OK;
+}
+
+void fill_result(mlstm_ctx* c, mlstm_step_result* out) {
+  const DevState& s = *c->st_host;
+  c->last = s;
+  c->have_last = true;
+  if (!out) return;
+  const double denom = (double)c->B * c->world * c->T;
+  out->loss_nats = s.loss_sum / denom;
+  out->bpc = out->loss_nats / std::log(2.0);
+  out->lr = s.lr_used;
+  out->loss_scale = s.alpha_used;
+  out->skipped = s.skipped;
+  out->step = s.it - 1;
+  out->applied = s.tau;
+}
+
+mlstm_status after_step(mlstm_ctx* c, mlstm_step_result* out) {
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  fill_result(c, out);
+  if (c->profile) {
+    float ms;
+    int prev = PH_PREP;
+    for (int p = PH_PREP + 1; p <= NPH; ++p) {
+      CUDA_OR_FAIL(c, cudaEventElapsedTime(&ms, c->ev[prev], c->ev[p]));
+      c->phase_ms[prev] += ms;
+      prev = p;
+    }
+  }
+  const DevState& s = *c->st_host;
+  if (!s.skipped && !std::isfinite(s.loss_sum)) {
+    if (++c->nonfinite_run >= c->cfg.diverge_patience)
+      return fail(MLSTM_EDIVERGED, "loss non-finite on diverge_patience consecutive applied steps");
+  } else {
+    c->nonfinite_run = 0;
+  }
+  return MLSTM_OK;
+}
+
+template <typename S>
+mlstm_status run_eval(mlstm_ctx* c, int Be, double* nats) {
+  Net<S>& n = net<S>(c);
+  RET_IF(enqueue_forward<S>(c, MLSTM_SLOT_EVAL));
+  LAUNCH(c, (ce_kernel<S><<<c->nblk_ce, 256, 0, c->stream>>>(n, Be, 0.f, 0)));
+  LAUNCH(c, (ce_reduce_kernel<S><<<1, 256, 0, c->stream>>>(n, c->nblk_ce, 0)));
+  LAUNCH(c, (state_out_kernel<S><<<grid_for((long)c->B * c->h), 256, 0, c->stream>>>(n, MLSTM_SLOT_EVAL)));
+  if (c->world > 1)
+    NCCL_OR_FAIL(c, ncclAllReduce(&c->st->loss_sum, &c->st->loss_sum, 1, ncclFloat64, ncclSum, c->comm, c->stream));
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(nats, &c->st->loss_sum, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  return MLSTM_OK;
+}
+
+float half_bits_to_float(uint16_t b) {
+  __half_raw r;
+  r.x = b;
+  return __half2float(__half(r));
+}
+
+// Copies `count` S elements at `dev` into host floats.
+mlstm_status read_floats(mlstm_ctx* c, const void* dev, long count, float* host) {
+  if (c->mixed) {
+    std::vector<uint16_t> tmp(count);
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(tmp.data(), dev, count * 2, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+    for (long i = 0; i < count; ++i) host[i] = half_bits_to_float(tmp[i]);
+  } else {
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(host, dev, count * 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  }
+  return MLSTM_OK;
+}
+
+mlstm_status write_floats(mlstm_ctx* c, void* dev, long count, const float* host) {
+  if (c->mixed) {
+    std::vector<uint16_t> tmp(count);
+    for (long i = 0; i < count; ++i) {
+      __half_raw r = __half(__float2half_rn(host[i]));
+      tmp[i] = r.x;
+    }
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(dev, tmp.data(), count * 2, cudaMemcpyHostToDevice, c->stream));
+  } else {
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(dev, host, count * 4, cudaMemcpyHostToDevice, c->stream));
+  }
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  return MLSTM_OK;
+}
+
+const void* hstate_ptr(mlstm_ctx* c) { return c->mixed ? (const void*)c->nh.hstate : (const void*)c->nf.hstate; }
+float* cstate_ptr(mlstm_ctx* c) { return c->mixed ? c->nh.cstate : c->nf.cstate; }
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+void mlstm_default_config(mlstm_config* cfg) {
+  if (!cfg) return;
+  memset(cfg, 0, sizeof *cfg);
+  cfg->hidden = 4096;
+  cfg->embed = 64;
+  cfg->vocab = 256;
+  cfg->seq_len = 256;
+  cfg->batch = 256;
+  cfg->micro_batch = 0;
+  cfg->precision = MLSTM_MIXED;
+  cfg->weight_norm = 0;
+  cfg->seed = 0x5EED;
+  cfg->lr0 = 3e-3;
+  cfg->decay_iters = 100000;
+  cfg->beta1 = 0.9;
+  cfg->beta2 = 0.999;
+  cfg->eps = 1e-8;
+  cfg->scale_init = 65536.f;
+  cfg->scale_min = 1.f;
+  cfg->scale_max = 16777216.f;
+  cfg->scale_growth_interval = 2000;
+  cfg->diverge_patience = 50;
+}
+
+int64_t mlstm_param_count(const mlstm_config* cfg) {
+  if (!cfg) return 0;
+  ParamOffsets po;
+  po.set(cfg->hidden, cfg->embed);
+  return po.P;
+}
+
+size_t mlstm_workspace_bytes(const mlstm_config* cfg) {
+  if (validate(cfg) != MLSTM_OK) return 0;
+  mlstm_ctx tmp;
+  set_dims(&tmp, cfg);
+  return layout_bytes(&tmp);
+}
+
+mlstm_status mlstm_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return fail(MLSTM_EINVAL, "null out");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(MLSTM_ENCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  memcpy(out, &id, 128);
+  return MLSTM_OK;
+}
+
+mlstm_status mlstm_init(const mlstm_config* cfg, void* workspace, size_t workspace_bytes, void* cuda_stream,
+                        const uint8_t* nccl_id, int rank, int world, mlstm_ctx** out) {
+  if (!out) return fail(MLSTM_EINVAL, "null out");
+  *out = nullptr;
+  RET_IF(validate(cfg));
+  if (world < 1 || rank < 0 || rank >= world) return fail(MLSTM_EINVAL, "bad rank/world");
+  if (world > 1 && !nccl_id) return fail(MLSTM_EINVAL, "nccl_id required when world > 1");
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255))
+    return fail(MLSTM_EINVAL, "workspace must be non-null and 256-byte aligned");
+  int dev = 0;
+  cudaDeviceProp prop;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess)
+    return fail(MLSTM_ECUDA, "no CUDA device");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(MLSTM_ECUDA, "libmlstm is built for sm_100a (B200); device is sm_" + std::to_string(prop.major) +
+                                 std::to_string(prop.minor));
+  mlstm_ctx* c = new mlstm_ctx();
+  set_dims(c, cfg);
+  const size_t need = layout_bytes(c);
+  if (workspace_bytes < need) {
+    delete c;
+    return fail(MLSTM_ENOMEM, "workspace too small: need " + std::to_string(need));
+  }
+  if (c->tc && !get_encoder()) {
+    delete c;
+    return fail(MLSTM_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  }
+  c->rank = rank;
+  c->world = world;
+  c->stream = static_cast<cudaStream_t>(cuda_stream);
+  c->ws = static_cast<uint8_t*>(workspace);
+  c->ws_bytes = workspace_bytes;
+  Carver cv{c->ws};
+  if (c->mixed) carve(c, cv, c->nh);
+  else carve(c, cv, c->nf);
+  auto bail = [&](mlstm_status s) {
+    mlstm_destroy(c);
+    return s;
+  };
+  if (cudaMallocHost(&c->st_host, sizeof(DevState)) != cudaSuccess) return bail(fail(MLSTM_ECUDA, "cudaMallocHost"));
+  if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(MLSTM_ECUDA, "cudaStreamCreate"));
+  for (int i = 0; i <= NPH; ++i)
+    if (cudaEventCreate(&c->ev[i]) != cudaSuccess) return bail(fail(MLSTM_ECUDA, "cudaEventCreate"));
+  // zero everything (pads of the transposed stashes must stay zero), then init
+  if (cudaMemsetAsync(c->ws, 0, need - 256, c->stream) != cudaSuccess) return bail(fail(MLSTM_ECUDA, "memset"));
+  DevState s0{};
+  s0.alpha = cfg->scale_init;
+  s0.alpha_used = cfg->scale_init;
+  if (cudaMemcpyAsync(c->st, &s0, sizeof s0, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+    return bail(fail(MLSTM_ECUDA, "memcpy state"));
+  float* master = c->mixed ? c->nh.master : c->nf.master;
+  init_params_kernel<<<grid_for(c->P), 256, 0, c->stream>>>(master, c->po, c->h, c->e, cfg->seed);
+  if (cudaGetLastError() != cudaSuccess) return bail(fail(MLSTM_ECUDA, "init kernel"));
+  mlstm_status s = c->mixed ? enqueue_cast<__half>(c) : enqueue_cast<float>(c);
+  if (s != MLSTM_OK) return bail(s);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(fail(MLSTM_ECUDA, "init sync"));
+  if (world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, 128);
+    ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess) return bail(fail(MLSTM_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)));
+  }
+  *out = c;
+  return MLSTM_OK;
+}
+
+mlstm_status mlstm_train_step(mlstm_ctx* c, const uint8_t* bytes, const uint8_t* reset, uint32_t flags,
+                              mlstm_step_result* out) {
+  RET_IF(ctx_ok(c));
+  if (!bytes) return fail(MLSTM_EINVAL, "null bytes");
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(c->bytes, bytes, (size_t)c->B * (c->T + 1), cudaMemcpyDeviceToDevice, c->stream));
+  if (reset) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->reset, reset, c->B, cudaMemcpyDeviceToDevice, c->stream));
+  else CUDA_OR_FAIL(c, cudaMemsetAsync(c->reset, 0, c->B, c->stream));
+  RET_IF(c->mixed ? run_train<__half>(c) : run_train<float>(c));
+  if (flags & MLSTM_ASYNC) return MLSTM_OK;
+  return after_step(c, out);
+}
+
+mlstm_status mlstm_train_step_host(mlstm_ctx* c, const uint8_t* bytes_host, const uint8_t* reset_host,
+                                   mlstm_step_result* out) {
+  RET_IF(ctx_ok(c));
+  if (!bytes_host) return fail(MLSTM_EINVAL, "null bytes");
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(c->bytes, bytes_host, (size_t)c->B * (c->T + 1), cudaMemcpyHostToDevice, c->stream));
+  if (reset_host) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->reset, reset_host, c->B, cudaMemcpyHostToDevice, c->stream));
+  else CUDA_OR_FAIL(c, cudaMemsetAsync(c->reset, 0, c->B, c->stream));
+  RET_IF(c->mixed ? run_train<__half>(c) : run_train<float>(c));
+  return after_step(c, out);
+}
+
+mlstm_status mlstm_eval(mlstm_ctx* c, const uint8_t* bytes, int32_t Be, const uint8_t* reset, double* nats_sum,
+                        int64_t* tokens, double* bpc) {
+  RET_IF(ctx_ok(c));
+  if (!bytes || Be <= 0 || Be > c->B) return fail(MLSTM_EINVAL, "eval needs bytes and 0 < Be <= batch");
+  CUDA_OR_FAIL(c, cudaMemsetAsync(c->bytes, 0, (size_t)c->B * (c->T + 1), c->stream));
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(c->bytes, bytes, (size_t)Be * (c->T + 1), cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_OR_FAIL(c, cudaMemsetAsync(c->reset, 0, c->B, c->stream));
+  if (reset) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->reset, reset, Be, cudaMemcpyDeviceToDevice, c->stream));
+  double nats = 0;
+  RET_IF(c->mixed ? run_eval<__half>(c, Be, &nats) : run_eval<float>(c, Be, &nats));
+  const int64_t tok = (int64_t)Be * c->T * c->world;
+  if (nats_sum) *nats_sum = nats;
+  if (tokens) *tokens = tok;
+  if (bpc) *bpc = nats / (double)tok / std::log(2.0);
+  return MLSTM_OK;
+}
+
+double mlstm_lr_at(double lr0, int64_t it, int64_t decay_iters) {
+  if (decay_iters <= 0) return 0.0;
+  return lr0 * std::fmax(0.0, 1.0 - (double)it / (double)decay_iters);
+}
+
+double mlstm_scale_lr(double base_lr, int rule, int64_t batch, int64_t ref_batch) {
+  if (ref_batch <= 0) ref_batch = 128;
+  const double r = (double)batch / (double)ref_batch;
+  switch (rule) {
+    case MLSTM_LR_LINEAR: return base_lr * r;
+    case MLSTM_LR_SQRT: return base_lr * std::sqrt(r);
+    default: return base_lr;
+  }
+}
+
+double mlstm_bpc_from_nats(double nats) { return nats / std::log(2.0); }
+
+mlstm_status mlstm_get_params(mlstm_ctx* c, float* host_out) {
+  RET_IF(ctx_ok(c));
+  if (!host_out) return fail(MLSTM_EINVAL, "null out");
+  float* master = c->mixed ? c->nh.master : c->nf.master;
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(host_out, master, sizeof(float) * c->P, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  return MLSTM_OK;
+}
+
+mlstm_status mlstm_set_params(mlstm_ctx* c, const float* host_in) {
+  RET_IF(ctx_ok(c));
+  if (!host_in) return fail(MLSTM_EINVAL, "null in");
+  float* master = c->mixed ? c->nh.master : c->nf.master;
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(master, host_in, sizeof(float) * c->P, cudaMemcpyHostToDevice, c->stream));
+  RET_IF(c->mixed ? enqueue_cast<__half>(c) : enqueue_cast<float>(c));
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  return MLSTM_OK;
+}
+
+mlstm_status mlstm_get_grads(mlstm_ctx* c, float* host_out) {
+  RET_IF(ctx_ok(c));
+  if (!host_out) return fail(MLSTM_EINVAL, "null out");
+  if (!c->have_last) return fail(MLSTM_ESTATE, "no train step has completed");
+  const void* arena = c->mixed ? (const void*)c->nh.arena : (const void*)c->nf.arena;
+  RET_IF(read_floats(c, arena, c->P, host_out));
+  const float inv = 1.f / c->last.alpha_used;
+  for (long i = 0; i < c->P; ++i) host_out[i] *= inv;
+  return MLSTM_OK;
+}
+
+mlstm_status mlstm_get_state(mlstm_ctx* c, int slot, float* h_out, float* c_out) {
+  RET_IF(ctx_ok(c));
+  if (slot != 0 && slot != 1) return fail(MLSTM_EINVAL, "bad slot");
+  const long BH = (long)c->B * c->h;
+  const size_t es = c->mixed ? 2 : 4;
+  if (h_out) RET_IF(read_floats(c, (const uint8_t*)hstate_ptr(c) + es * slot * BH, BH, h_out));
+  if (c_out) {
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(c_out, cstate_ptr(c) + slot * BH, 4 * BH, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  }
+  return MLSTM_OK;
+}
+
+mlstm_status mlstm_set_state(mlstm_ctx* c, int slot, const float* h_in, const float* c_in) {
+  RET_IF(ctx_ok(c));
+  if (slot != 0 && slot != 1) return fail(MLSTM_EINVAL, "bad slot");
+  const long BH = (long)c->B * c->h;
+  const size_t es = c->mixed ? 2 : 4;
+  if (h_in) RET_IF(write_floats(c, (uint8_t*)hstate_ptr(c) + es * slot * BH, BH, h_in));
+  if (c_in) {
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(cstate_ptr(c) + slot * BH, c_in, 4 * BH, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  }
+  return MLSTM_OK;
+}
+
+mlstm_status mlstm_get_opt_state(mlstm_ctx* c, float* m_out, float* v_out, int64_t* tau, float* alpha,
+                                 int32_t* clean_steps, int64_t* it) {
+  RET_IF(ctx_ok(c));
+  if (m_out) CUDA_OR_FAIL(c, cudaMemcpyAsync(m_out, c->adam_m, 4 * c->P, cudaMemcpyDeviceToHost, c->stream));
+  if (v_out) CUDA_OR_FAIL(c, cudaMemcpyAsync(v_out, c->adam_v, 4 * c->P, cudaMemcpyDeviceToHost, c->stream));
+  DevState s;
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(&s, c->st, sizeof s, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  if (tau) *tau = s.tau;
+  if (alpha) *alpha = s.alpha;
+  if (clean_steps) *clean_steps = s.clean;
+  if (it) *it = s.it;
+  return MLSTM_OK;
+}
+
+mlstm_status mlstm_set_opt_state(mlstm_ctx* c, const float* m_in, const float* v_in, int64_t tau, float alpha,
+                                 int32_t clean_steps, int64_t it) {
+  RET_IF(ctx_ok(c));
+  if (!(alpha >= c->cfg.scale_min && alpha <= c->cfg.scale_max) || tau < 0 || it < 0 || clean_steps < 0)
+    return fail(MLSTM_EINVAL, "bad optimiser state");
+  if (m_in) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->adam_m, m_in, 4 * c->P, cudaMemcpyHostToDevice, c->stream));
+  if (v_in) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->adam_v, v_in, 4 * c->P, cudaMemcpyHostToDevice, c->stream));
+  DevState s;
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(&s, c->st, sizeof s, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  s.tau = tau;
+  s.alpha = alpha;
+  s.clean = clean_steps;
+  s.it = it;
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(c->st, &s, sizeof s, cudaMemcpyHostToDevice, c->stream));
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  return MLSTM_OK;
+}
+
+mlstm_status mlstm_debug_dump(mlstm_ctx* c, const char* name, float* host_out, size_t n) {
+  RET_IF(ctx_ok(c));
+  if (!name || !host_out) return fail(MLSTM_EINVAL, "null argument");
+  const long B = c->B, T = c->T, h = c->h, e = c->e;
+  const std::string nm(name);
+  auto need = [&](long k) { return (size_t)k <= n; };
+  if (nm == "x") {
+    const long cnt = T * B * e;
+    if (!need(cnt)) return fail(MLSTM_EINVAL, "buffer too small");
+    float* tmp = nullptr;
+    CUDA_OR_FAIL(c, cudaMalloc(&tmp, cnt * 4));
+    if (c->mixed) gather_x_kernel<__half><<<grid_for(cnt), 256, 0, c->stream>>>(c->nh, tmp);
+    else gather_x_kernel<float><<<grid_for(cnt), 256, 0, c->stream>>>(c->nf, tmp);
+    cudaError_t e1 = cudaMemcpyAsync(host_out, tmp, cnt * 4, cudaMemcpyDeviceToHost, c->stream);
+    cudaError_t e2 = cudaStreamSynchronize(c->stream);
+    cudaFree(tmp);
+    CUDA_OR_FAIL(c, e1);
+    CUDA_OR_FAIL(c, e2);
+    return MLSTM_OK;
+  }
+  if (nm == "logits" || nm == "loss_rows" || nm == "c" || nm == "tab") {
+    const float* src;
+    long cnt;
+    if (nm == "logits") src = c->mixed ? c->nh.Y : c->nf.Y, cnt = T * B * 256;
+    else if (nm == "loss_rows") src = c->mixed ? c->nh.lossrow : c->nf.lossrow, cnt = T * B;
+    else if (nm == "c") src = (c->mixed ? c->nh.Crm : c->nf.Crm) + B * h, cnt = T * B * h;
+    else src = c->mixed ? c->nh.tab : c->nf.tab, cnt = 256 * 5 * h;
+    if (!need(cnt)) return fail(MLSTM_EINVAL, "buffer too small");
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(host_out, src, cnt * 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+    return MLSTM_OK;
+  }
+  if (nm == "h") {
+    const long cnt = T * B * h;
+    if (!need(cnt)) return fail(MLSTM_EINVAL, "buffer too small");
+    const size_t es = c->mixed ? 2 : 4;
+    const void* src = c->mixed ? (const void*)c->nh.Hrm : (const void*)c->nf.Hrm;
+    return read_floats(c, (const uint8_t*)src + es * B * h, cnt, host_out);
+  }
+  if (nm == "onehot") {  // [256][T][B]
+    const long cnt = 256 * T * B;
+    if (!need(cnt)) return fail(MLSTM_EINVAL, "buffer too small");
+    std::vector<float> row(c->ldK);
+    const size_t es = c->mixed ? 2 : 4;
+    const uint8_t* base = c->mixed ? (const uint8_t*)c->nh.OHT : (const uint8_t*)c->nf.OHT;
+    for (int v = 0; v < 256; ++v) {
+      RET_IF(read_floats(c, base + es * v * c->ldK, c->ldK, row.data()));
+      for (long t = 0; t < T; ++t)
+        for (long b = 0; b < B; ++b) host_out[(v * T + t) * B + b] = row[t * c->Bp + b];
+    }
+    return MLSTM_OK;
+  }
+  return fail(MLSTM_EINVAL, "unknown dump name");
+}
+
+mlstm_status mlstm_check_overflow(mlstm_ctx* c, const void* device_buf, int64_t n, int dtype, int32_t* flag) {
+  RET_IF(ctx_ok(c));
+  if (!device_buf || !flag || n < 0 || (dtype != 0 && dtype != 1)) return fail(MLSTM_EINVAL, "bad arguments");
+  CUDA_OR_FAIL(c, cudaMemsetAsync(c->scratch_flag, 0, 4, c->stream));
+  if (dtype == 0)
+    overflow_kernel<__half><<<grid_for(n), 256, 0, c->stream>>>((const __half*)device_buf, n, c->scratch_flag);
+  else
+    overflow_kernel<float><<<grid_for(n), 256, 0, c->stream>>>((const float*)device_buf, n, c->scratch_flag);
+  CUDA_OR_FAIL(c, cudaGetLastError());
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(flag, c->scratch_flag, 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  return MLSTM_OK;
+}
+
+mlstm_status mlstm_profile_enable(mlstm_ctx* c, int enable) {
+  RET_IF(ctx_ok(c));
+  if ((enable != 0) != c->profile) {
+    c->profile = enable != 0;
+    if (c->gA) cudaGraphExecDestroy(c->gA);
+    if (c->gB) cudaGraphExecDestroy(c->gB);
+    c->gA = c->gB = nullptr;
+  }
+  memset(c->phase_ms, 0, sizeof c->phase_ms);
+  return MLSTM_OK;
+}
+
+mlstm_status mlstm_phase_times(mlstm_ctx* c, double* ms_out, int32_t* launches_out, int32_t* n_phases) {
+  RET_IF(ctx_ok(c));
+  if (n_phases) *n_phases = NPH;
+  for (int i = 0; i < NPH; ++i) {
+    if (ms_out) ms_out[i] = c->phase_ms[i];
+    if (launches_out) launches_out[i] = c->phase_launches[i];
+  }
+  return MLSTM_OK;
+}
+
+const char* mlstm_phase_name(int phase) { return (phase >= 0 && phase < NPH) ? kPhaseNames[phase] : ""; }
+
+int32_t mlstm_launches_per_step(mlstm_ctx* c) {
+  if (!c) return 0;
+  if (!c->gA) {
+    mlstm_status s = c->mixed ? build_graphs<__half>(c) : build_graphs<float>(c);
+    if (s != MLSTM_OK) return -1;
+  }
+  return c->launches;
+}
+
+const char* mlstm_last_error(void) { return g_err.c_str(); }
+
+void mlstm_destroy(mlstm_ctx* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->gA) cudaGraphExecDestroy(c->gA);
+  if (c->gB) cudaGraphExecDestroy(c->gB);
+  for (int i = 0; i <= NPH; ++i)
+    if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+  if (c->st_host) cudaFreeHost(c->st_host);
+  if (c->cap) cudaStreamDestroy(c->cap);
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+}
+
+}  // extern "C"

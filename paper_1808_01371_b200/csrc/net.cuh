@@ -1,0 +1,147 @@
+// net.cuh -- device view of the step's HBM layout and the small helpers every kernel shares.
+//
+// Notation follows the paper / SURVEY §8a: h hidden width, e embedding width, B rows per rank,
+// T TBTT window, S the storage type (__half in mixed mode, float in fp32 mode).
+//
+// Internal gate order.  The 4h gate rows of W_h / W_x (canonical order i | f | o | u, each h rows)
+// are stored interleaved in blocks of 16 units: internal row r = (j/16)*64 + g*16 + j%16 for gate
+// g in {i,f,o,u} and unit j.  A 64-column chunk of any gate-producing GEMM therefore holds all
+// four gates of 16 units, so the gate nonlinearity and cell update fuse into that GEMM's
+// epilogue with no cross-thread exchange (one TMEM lane = one batch row).
+#pragma once
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+namespace mlstm {
+
+__host__ __device__ __forceinline__ int int_row(int g, int j) { return (j >> 4) * 64 + g * 16 + (j & 15); }
+__host__ __device__ __forceinline__ int canon_of_int(int r, int h) {
+  return ((r >> 4) & 3) * h + (r >> 6) * 16 + (r & 15);
+}
+
+// Canonical flat parameter offsets (include/mlstm.h).
+struct ParamOffsets {
+  long E, Wmx, Wmh, Wx, Wh, b, Wdec, bdec, P;
+  __host__ __device__ void set(int h, int e) {
+    E = 0;
+    Wmx = E + 256L * e;
+    Wmh = Wmx + (long)h * e;
+    Wx = Wmh + (long)h * h;
+    Wh = Wx + 4L * h * e;
+    b = Wh + 4L * h * h;
+    Wdec = b + 4L * h;
+    bdec = Wdec + 256L * h;
+    P = bdec + 256;
+  }
+};
+
+// Device-resident scalar state: loss-scale state machine, LR clock and Adam count (Q10).
+struct DevState {
+  double loss_sum;     // global sum of per-position CE of the last step (after allreduce)
+  double lr_used;      // LR the last step used
+  float alpha;         // current loss scale
+  float alpha_used;    // loss scale the last step's backward used
+  int32_t overflow;    // set by the overflow scan of the reduced gradients
+  int32_t clean;       // clean steps since the last growth / backoff
+  int64_t it;          // LR clock: advances every step (incl. skipped)
+  int64_t tau;         // applied Adam updates
+  int32_t skipped;     // last step skipped?
+  int32_t pad;
+};
+
+template <typename S>
+struct Net {
+  int h, e, B, T, Bp;
+  long ldK;  // leading dim of the transposed stashes over K = T*Bp (padded to 64)
+  long ldH;  // leading dim of HT over (T+1)*Bp
+  ParamOffsets po;
+  const uint8_t* bytes;  // [B][T+1]
+  const uint8_t* reset;  // [B] or null
+  float* master;         // fp32 masters, canonical (biases are read from here)
+  S* arena;              // gradient buckets, canonical layout (fp16 in mixed mode)
+  // fp16 (S) working copies
+  S *E_w, *Wcat_w, *Wmh_w, *Wh_w, *Wdec_w, *WmhT, *WhT, *WdecT;
+  // activations / stash
+  float* tab;     // [256][5h]: cols [0,h) = W_mx E^T (mx table), [h,5h) = W_x E^T in internal order
+  S* Hrm;         // [(T+1)][B][h]; block 0 = h0, block t+1 = H_t
+  S* HT;          // [h][ldH]; column t*Bp+b = Hrm[t][b]
+  float* Crm;     // [(T+1)][B][h]
+  S* Mscr;        // [B][h]   m_t of the current step (A operand of the W_h GEMM)
+  S* MT;          // [h][ldK] m_t^T stash (B operand of dW_h)
+  S* Astash;      // [T][B][h] a_t = W_mh h_{t-1}
+  S* Gates;       // [T][B][4h] i,f,o,u activations, internal order
+  float* Y;       // [T*B][256] logits (fp32)
+  float* lossrow; // [T*B]
+  S* dY;          // [T*B][256]
+  S* dYT;         // [256][ldK]
+  S* OHT;         // [256][ldK] one-hot of the input bytes, transposed
+  float* dHdec;   // [T*B][h]
+  S* dZscr;       // [B][4h] internal order
+  S* dAscr;       // [B][h]
+  float* dC;      // [B][h] dc carry
+  S* dGT;         // [5h][ldK]: rows [0,h) dMX^T, rows [h,5h) dZ^T (internal)
+  S* dAT;         // [h][ldK]
+  float* part;    // split-K partials
+  float* Scan;    // [256][5h] per-byte segmented sums, canonical columns
+  S* hstate;      // [2][B][h]  persisted h per slot
+  float* cstate;  // [2][B][h]  persisted c per slot
+  double* loss_part;
+  float* colsum_part;
+  DevState* st;
+  __device__ __forceinline__ int byte_at(int b, int t) const { return bytes[(long)b * (T + 1) + t]; }
+  __device__ __forceinline__ long kcol(int t, int b) const { return (long)t * Bp + b; }
+};
+
+template <typename S>
+__device__ __forceinline__ S to_s(float x);
+template <>
+__device__ __forceinline__ __half to_s<__half>(float x) {
+  return __float2half_rn(x);
+}
+template <>
+__device__ __forceinline__ float to_s<float>(float x) {
+  return x;
+}
+__device__ __forceinline__ float to_f(__half x) { return __half2float(x); }
+__device__ __forceinline__ float to_f(float x) { return x; }
+
+// Contiguous stores / loads of 16 values (rows are 16-element aligned by construction).
+__device__ __forceinline__ void st16(__half* dst, const float* v) {
+  uint4 w[2];
+  __half2* p = reinterpret_cast<__half2*>(w);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p[i] = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+  reinterpret_cast<uint4*>(dst)[0] = w[0];
+  reinterpret_cast<uint4*>(dst)[1] = w[1];
+}
+__device__ __forceinline__ void st16(float* dst, const float* v) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+}
+__device__ __forceinline__ void ld16(const __half* src, float* v) {
+  uint4 w[2];
+  w[0] = reinterpret_cast<const uint4*>(src)[0];
+  w[1] = reinterpret_cast<const uint4*>(src)[1];
+  const __half2* p = reinterpret_cast<const __half2*>(w);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float2 f = __half22float2(p[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void ld16(const float* src, float* v) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float4 f = reinterpret_cast<const float4*>(src)[i];
+    v[4 * i] = f.x;
+    v[4 * i + 1] = f.y;
+    v[4 * i + 2] = f.z;
+    v[4 * i + 3] = f.w;
+  }
+}
+
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-x)); }
+
+}  // namespace mlstm

@@ -1,0 +1,220 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on identical seeded inputs.
+
+Sizes span several tiles and a ragged tail (B = 130 > 128 rows, h = 128 > 64 columns) and the
+BASELINE.json parity configs C1 (h=64, T=16, B=4) and C2 (h=1024, T=64, B=128).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import mlstm_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a B200", allow_module_level=True)
+
+from gpu_helpers import (TOL, compare_grads, inputs, make_model, oracle_step, rel_l2, split,  # noqa: E402
+                         to_dev)
+
+CASES = [
+    # (name, h, e, B, T)
+    ("C1", 64, 64, 4, 16),
+    ("ragged", 128, 64, 130, 5),
+    ("C2", 1024, 64, 128, 64),
+]
+
+
+@pytest.mark.parametrize("precision", ["fp32", "mixed"])
+def test_init_matches_oracle_bitwise(precision):
+    h, e = 128, 64
+    m = make_model(h, e, 8, 4, precision, seed=1234)
+    got = m.get_params()
+    ref = O.flatten(O.init_params(h, e, 1234)).astype(np.float32)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "mixed"])
+@pytest.mark.parametrize("name,h,e,B,T", CASES)
+def test_train_step_parity(name, h, e, B, T, precision):
+    m = make_model(h, e, B, T, precision)
+    theta0 = m.get_params().astype(np.float64)
+    by = inputs(B, T)
+    res = m.train_step(to_dev(by))
+    loss_ref, g_ref, (hT, cT), _ = oracle_step(theta0, by, h, e)
+    loss_rel = abs(res["loss_nats"] - loss_ref) / abs(loss_ref)
+    g = m.get_grads().astype(np.float64)
+    rep = compare_grads(g, g_ref, h, e, precision)
+    tol = TOL[precision]
+    assert loss_rel <= tol["loss_rel"], (loss_rel, res, loss_ref)
+    assert res["skipped"] == 0 and res["step"] == 0 and res["applied"] == 1
+    assert abs(res["bpc"] - res["loss_nats"] / math.log(2)) < 1e-12
+    for n, v in rep.items():
+        if precision == "fp32":
+            assert v <= tol["grad_rel_l2"], (n, v, rep)
+        else:
+            assert v >= tol["grad_cos"], (n, v, rep)
+    # persisted state = final (h, c) of the window
+    hs, cs = m.get_state(0)
+    htol = 1e-5 if precision == "fp32" else 2e-3
+    assert np.abs(hs - hT).max() <= htol and np.abs(cs - cT).max() <= 10 * htol
+    # the Adam update the GPU applied equals the oracle's Adam on the GPU's own gradients
+    theta1 = m.get_params().astype(np.float64)
+    st = O.AdamState(np.zeros_like(theta0), np.zeros_like(theta0))
+    th_ref, _ = O.adam_apply(theta0, g, st, O.lr_at(3e-3, 0, 100_000))
+    upd, upd_ref = theta1 - theta0, th_ref - theta0
+    assert rel_l2(upd, upd_ref) < 1e-3
+
+
+def test_multi_step_trace_fp32_tracks_oracle():
+    """10 steps (forward, BPTT, scaler, Adam, schedule, persisted state) vs the oracle loop."""
+    h, e, B, T = 64, 64, 4, 16
+    m = make_model(h, e, B, T, "fp32")
+    st = O.new_train_state(h, e, B, seed=0x5EED)
+    assert np.array_equal(st.theta.astype(np.float32), m.get_params())
+    for k in range(10):
+        by = inputs(B, T, k=k)
+        r = m.train_step(to_dev(by))
+        ro = O.train_step(st, by)
+        assert abs(r["loss_nats"] - ro["loss_nats"]) <= 1e-4 * ro["loss_nats"], (k, r, ro)
+        assert r["lr"] == pytest.approx(ro["lr"], rel=1e-12) and r["loss_scale"] == ro["alpha"]
+        assert bool(r["skipped"]) == ro["skipped"]
+    assert rel_l2(m.get_params().astype(np.float64), st.theta) < 1e-4
+
+
+@pytest.mark.parametrize("precision", ["fp32", "mixed"])
+def test_byte_indexing_bit_exact(precision):
+    h, e, B, T = 64, 64, 6, 9
+    m = make_model(h, e, B, T, precision)
+    # a tiny W_dec (logit noise ~1e-5) and distinct b_dec make the 256 logits of every row distinct
+    # by ~1e-2, so the target index of each per-position loss is identifiable from its value
+    P = split(m.get_params(), h, e)
+    P["W_dec"] *= 1e-3
+    P["b_dec"][:] = np.arange(256) * 1e-2
+    m.set_params(O.flatten(P))
+    by = inputs(B, T, kind="uniform")
+    m.train_step(to_dev(by))
+    # X = E_w[bytes] exactly as the kernels index it
+    x = m.debug_dump("x", T * B * e).reshape(T, B, e)
+    E = m.get_params()[: 256 * e].reshape(256, e)  # masters after the update == E_w's source
+    # one-hot of the input bytes (drives S = onehot^T dG, i.e. dE, dW_x, dW_mx, db)
+    oh = m.debug_dump("onehot", 256 * T * B).reshape(256, T, B)
+    ref = (np.arange(256)[:, None, None] == by[:, :T].T[None]).astype(np.float32)
+    assert np.array_equal(oh, ref)
+    # target shift: each per-position loss equals lse(y) - y[bytes[b, t+1]] and no other index
+    y = m.debug_dump("logits", T * B * 256).reshape(T, B, 256).astype(np.float64)
+    lr = m.debug_dump("loss_rows", T * B).reshape(T, B).astype(np.float64)
+    lse = np.log(np.exp(y - y.max(-1, keepdims=True)).sum(-1)) + y.max(-1)
+    cand = lse[..., None] - y
+    best = np.abs(cand - lr[..., None]).argmin(-1)
+    assert np.array_equal(best, by[:, 1:].T)
+    # dE support: nonzero rows exactly the bytes used as inputs
+    g = split(m.get_grads(), h, e)
+    nz = set(np.nonzero(np.abs(g["E"]).sum(1))[0].tolist())
+    assert nz == set(by[:, :T].ravel().tolist())
+    # X rows equal the working copy of E (fp16 RNE of the masters in mixed mode) at those bytes
+    Ew = E.astype(np.float16).astype(np.float32) if precision == "mixed" else E
+    assert np.array_equal(x, Ew[by[:, :T].T])
+
+
+def test_overflow_predicate_bit_exact():
+    m = make_model(64, 64, 4, 4, "mixed")
+    rng = np.random.default_rng(0)
+    for trial in range(20):
+        n = int(rng.integers(1, 5000))
+        vals = rng.standard_normal(n) * 1000
+        k = int(rng.integers(0, 4))
+        for _ in range(k):
+            vals[rng.integers(0, n)] = rng.choice([65504.0, 65519.99, 65520.0, -65520.0, np.inf, np.nan, 7e4])
+        h16 = O.to_fp16(vals)
+        t16 = torch.from_numpy(h16).cuda()
+        assert m.check_overflow(t16) == O.overflow(h16)
+        t32 = torch.from_numpy(vals.astype(np.float32)).cuda()
+        assert m.check_overflow(t32) == O.overflow(vals.astype(np.float32))
+
+
+def test_loss_scale_overflow_decisions_and_replay():
+    """alpha = 2^24 must overflow the fp16 gradients at this size, alpha = 1 must not (far from the
+    threshold); the GPU's alpha trace equals the oracle scaler replayed on the GPU's
+    overflow flags."""
+    h, e, B, T = 64, 64, 4, 16
+    m = make_model(h, e, B, T, "mixed", scale_growth_interval=2)
+    st = O.ScalerState(alpha=2.0 ** 24, growth_interval=2)
+    m.set_opt_state(alpha=2.0 ** 24)
+    theta = m.get_params()
+    skipped = []
+    for k in range(8):
+        r = m.train_step(to_dev(inputs(B, T, k=k)))
+        assert r["loss_scale"] == st.alpha
+        apply, st = O.scaler_step(st, bool(r["skipped"]))
+        skipped.append(r["skipped"])
+        if r["skipped"]:
+            assert np.array_equal(m.get_params(), theta)
+        theta = m.get_params()
+    assert skipped[0] == 1
+    assert m.get_opt_state()["alpha"] == st.alpha
+    m2 = make_model(h, e, B, T, "mixed")
+    m2.set_opt_state(alpha=1.0)
+    assert m2.train_step(to_dev(inputs(B, T)))["skipped"] == 0
+
+
+@pytest.mark.parametrize("precision", ["fp32", "mixed"])
+def test_eval_matches_oracle(precision):
+    h, e, B, T = 128, 64, 16, 12
+    m = make_model(h, e, B, T, precision)
+    P = split(m.get_params(), h, e)
+    by = inputs(B, T, kind="markov")
+    nats, tok, bpc = m.eval(to_dev(by))
+    ref, tok_ref, _ = O.evaluate(P, by, np.zeros((B, h)), np.zeros((B, h)))
+    assert tok == tok_ref
+    tol = 1e-5 if precision == "fp32" else 5e-3
+    assert abs(nats - ref) / ref <= tol
+    assert abs(bpc - O.bpc_from_nats(ref / tok)) <= tol * 8
+
+
+def test_state_carry_two_windows_bitwise():
+    """Eval over [T] then [T] with persisted state == the state after the same bytes in one model
+    run twice (determinism) and equals the oracle's carried state."""
+    h, e, B, T = 128, 64, 8, 6
+    s = inputs(B, 2 * T)
+    w1, w2 = s[:, :T + 1], s[:, T:]
+    outs = []
+    for _ in range(2):
+        m = make_model(h, e, B, T, "fp32")
+        m.eval(to_dev(w1))
+        m.eval(to_dev(w2))
+        outs.append(m.get_state(1))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    P = split(m.get_params(), h, e)
+    _, _, (hT, cT) = O.forward(P, s, np.zeros((B, h)), np.zeros((B, h)))
+    assert np.abs(outs[0][0] - hT).max() < 1e-5
+
+
+def test_reset_rows_start_from_zero_state():
+    h, e, B, T = 64, 64, 4, 8
+    m = make_model(h, e, B, T, "fp32")
+    rng = np.random.default_rng(3)
+    h0, c0 = rng.standard_normal((B, h)).astype(np.float32), rng.standard_normal((B, h)).astype(np.float32)
+    m.set_state(h0, c0)
+    by = inputs(B, T)
+    reset = np.array([0, 1, 0, 1], dtype=np.uint8)
+    theta0 = m.get_params().astype(np.float64)
+    r = m.train_step(to_dev(by), to_dev(reset))
+    h0r, c0r = h0.astype(np.float64), c0.astype(np.float64)
+    h0r[reset == 1] = 0
+    c0r[reset == 1] = 0
+    loss_ref, _, _, _ = oracle_step(theta0, by, h, e, h0r, c0r)
+    assert abs(r["loss_nats"] - loss_ref) / loss_ref < 1e-5
+
+
+def test_host_entry_point_matches_device_entry_point():
+    h, e, B, T = 64, 64, 4, 16
+    by = inputs(B, T)
+    a = make_model(h, e, B, T, "mixed")
+    b = make_model(h, e, B, T, "mixed")
+    ra = a.train_step(to_dev(by))
+    rb = b.train_step_host(by)
+    assert ra == rb
+    assert np.array_equal(a.get_params(), b.get_params())
