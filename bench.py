@@ -118,33 +118,42 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+class OracleSampler:
+    """The fp64 oracle as it stands, timed on a bounded sample of the same workload (same h, e; 32 rows;
+    window length sized so one sample is ~seconds_hint of CPU work): forward, BPTT and Adam."""
+
+    def __init__(self, h, e, seconds_hint=15.0, B=32):
+        from oracle import mlstm_oracle as O
+        from synth import bytestream
+        self.O, self.h, self.e, self.B = O, h, e, B
+        self.cores = len(os.sched_getaffinity(0))
+        self.P = O.init_params(h, e, 0x5EED)
+        self.theta = O.flatten(self.P)
+        # Per timestep the oracle streams every fp64 weight matrix a few times, so its cost is nearly
+        # flat in the row count: calibrate on a short window, then size the window.
+        by = bytestream.window(np.arange(B), 0, 4)
+        z = np.zeros((B, h))
+        t0 = time.perf_counter()
+        O.loss_and_grads(self.P, by, z, z)
+        per_step = (time.perf_counter() - t0) / 4
+        self.T = int(max(4, min(256, seconds_hint / max(per_step, 1e-4))))
+        self.by = bytestream.window(np.arange(B), 0, self.T)
+
+    def run(self):
+        O, B, h = self.O, self.B, self.h
+        z = np.zeros((B, h))
+        t0 = time.perf_counter()
+        _, g, _, _ = O.loss_and_grads(self.P, self.by, z, z)
+        st = O.AdamState(np.zeros_like(self.theta), np.zeros_like(self.theta))
+        O.adam_apply(self.theta, O.flatten(g), st, 3e-3)
+        dt = time.perf_counter() - t0
+        return {"value": B * self.T / dt, "unit": "chars/s", "cores": self.cores, "kind": "oracle",
+                "sample": f"fp64 NumPy oracle, h={h} e={self.e}, {B} rows x T={self.T} window (forward, BPTT, "
+                          f"Adam), {dt:.1f} s on {self.cores} host threads"}
+
+
 def cpu_baseline(h, e, seconds_hint=15.0):
-    """The fp64 oracle as it stands, on a bounded sample of the same workload (same h, e, T=128 window,
-    B rows chosen so the sample is ~10-30 s of CPU work): forward, BPTT and Adam."""
-    from oracle import mlstm_oracle as O
-    from synth import bytestream
-    cores = len(os.sched_getaffinity(0))
-    P = O.init_params(h, e, 0x5EED)
-    theta = O.flatten(P)
-    T = 128 if h >= 2048 else 64
-    B = 1
-    # calibrate on one row, then scale the row count toward the time hint
-    t0 = time.perf_counter()
-    by = bytestream.window(np.arange(B), 0, T)
-    z = np.zeros((B, h))
-    O.loss_and_grads(P, by, z, z)
-    dt1 = time.perf_counter() - t0
-    B = int(max(1, min(64, seconds_hint / max(dt1, 1e-3))))
-    by = bytestream.window(np.arange(B), 0, T)
-    z = np.zeros((B, h))
-    t0 = time.perf_counter()
-    _, g, _, _ = O.loss_and_grads(P, by, z, z)
-    st = O.AdamState(np.zeros_like(theta), np.zeros_like(theta))
-    O.adam_apply(theta, O.flatten(g), st, 3e-3)
-    dt = time.perf_counter() - t0
-    return {"value": B * T / dt, "unit": "chars/s", "cores": cores, "kind": "oracle",
-            "sample": f"fp64 NumPy oracle, h={h} e={e}, {B} rows x T={T} window (forward, BPTT, Adam), "
-                      f"{dt:.1f} s on {cores} host threads"}
+    return OracleSampler(h, e, seconds_hint).run()
 
 
 def dist_env():
@@ -156,10 +165,12 @@ def run_reference(args):
     if rank != 0:
         return
     h, e, B, T, desc = CONFIGS[args.config]
-    # each "step" is one bounded sample of the workload on the host cores
+    # each "step" is one bounded sample of the workload on the host cores; the whole run stays
+    # within a few minutes
+    sampler = OracleSampler(h, e, seconds_hint=min(args.ref_seconds, 150.0 / (args.warmup + args.steps)))
     vals = []
     for i in range(args.warmup + args.steps):
-        r = cpu_baseline(h, e, seconds_hint=args.ref_seconds)
+        r = sampler.run()
         if i >= args.warmup:
             vals.append(r["value"])
     v = float(np.median(vals))

@@ -133,6 +133,139 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// gemm_tc2_kernel: the same contract with a CTA pair (cluster of 2, tcgen05 cta_group::2) per
+// 256 x BN output tile.  Each CTA stages its 128 rows of A and BN/2 rows of B per k-block, so a
+// CTA pulls (128 + BN/2) x 64 x 2 bytes per 256 x BN x 64 of MMA work: half the operand traffic per
+// FLOP of the 1-CTA tile -- the L2 -> SM path is what bounds these GEMMs.  Both CTAs' TMA loads
+// count on the leader's full barrier; the leader's single thread issues the M=256 MMA; its commit
+// multicasts to both CTAs' empty / accumulator barriers; each CTA's epilogue reads its own TMEM.
+template <int BN>
+struct Tc2Cfg {
+  static constexpr int BM = 128, BK = 64;  // rows per CTA
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN == 256 ? 6 : (BN == 128 ? 8 : 10);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int BN, class Epi>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                    int N, int K, int az, int bz, int kb_per_split, Epi epi) {
+  using C = Tc2Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* accf = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int n0 = (blockIdx.x >> 1) * BN;
+  const int m0 = blockIdx.y * 256 + rank * 128;
+  const int total_kb = (K + C::BK - 1) / C::BK;
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int nkb = max(0, min(kb_per_split, total_kb - kb0));
+
+  if (threadIdx.x == 0) {
+#pragma unroll 1
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);   // leader's arrive.expect_tx covers both CTAs' bytes
+      ptx::mbar_init(&empty[s], 1);  // leader's multicast commit
+    }
+    ptx::mbar_init(accf, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc2(tmem_slot, BN);
+    ptx::tmem_relinquish2();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && nkb > 0) {
+      const uint64_t pol = ptx::policy_evict_last();
+      const uint32_t full_leader0 = ptx::mapa_shared(ptx::smem_u32(&full[0]), 0);
+#pragma unroll 1
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % C::STAGES;
+        const uint32_t ph = (i / C::STAGES) & 1;
+        ptx::mbar_wait(&empty[s], ph ^ 1);
+        // Only the leader arrives (with both CTAs' byte count).  The peer's bytes may land first and
+        // drive the tx-count transiently negative; the phase cannot complete before the leader's
+        // arrive, and the peer cannot run a phase ahead (it waits on its own empty barrier, released
+        // by the same commit).  A release.cluster remote arrive here would fence every prior TMA.
+        if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * C::STAGE_BYTES);
+        const int kc = (kb0 + i) * C::BK;
+        ptx::tma_load_3d_2sm(sA + s * C::A_BYTES, &tmA, full_leader0 + s * 8, kc, m0, az, pol);
+        ptx::tma_load_3d_2sm(sB + s * C::B_BYTES, &tmB, full_leader0 + s * 8, kc, n0 + rank * (BN / 2), bz, pol);
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0 && nkb > 0) {
+      constexpr uint32_t idesc = ptx::idesc_f16_f32(256, BN);
+#pragma unroll 1
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % C::STAGES;
+        const uint32_t ph = (i / C::STAGES) & 1;
+        ptx::mbar_wait(&full[s], ph);
+        ptx::tc_fence_after();
+        const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
+        const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
+#pragma unroll
+        for (int k = 0; k < C::BK / 16; ++k)
+          ptx::mma_f16_2sm(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
+        ptx::mma_commit_2sm_mc(&empty[s], 0x3);
+      }
+      ptx::mma_commit_2sm_mc(accf, 0x3);
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = m0 + q * 32 + lane;
+    if (nkb > 0) {
+      ptx::mbar_wait(accf, 0);
+      ptx::tc_fence_after();
+    }
+#pragma unroll 1
+    for (int c = 0; c < BN / 64; ++c) {
+      float v[64];
+      if (nkb > 0) {
+        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 64;
+        ptx::tmem_ld16(ta, v);
+        ptx::tmem_ld16(ta + 16, v + 16);
+        ptx::tmem_ld16(ta + 32, v + 32);
+        ptx::tmem_ld16(ta + 48, v + 48);
+        ptx::tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) v[i] = 0.f;
+      }
+      const int col0 = n0 + c * 64;
+      if (row < M && col0 < N) epi(row, col0, v);
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc2(tmem, BN);
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ float ld_as_float(const T* p) {
   return static_cast<float>(*p);

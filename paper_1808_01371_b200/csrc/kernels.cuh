@@ -301,45 +301,85 @@ __global__ void wgrad_finalize_kernel(Net<S> n, const float* __restrict__ part, 
   }
 }
 
-// dW_mx = S_mx^T E, dW_x = S_x^T E  (X = E[bytes] so dZ^T X = sum_v S[v]^T E[v]); fp32 accumulate.
-template <typename S>
-__global__ void dwcat_kernel(Net<S> n) {
-  const int h = n.h, e = n.e;
-  const int r = blockIdx.x * blockDim.y + threadIdx.y;  // canonical row of [W_mx; W_x], < 5h
-  if (r >= 5 * h) return;
-  for (int c = threadIdx.x; c < e; c += blockDim.x) {
+// Small fp32 SIMT GEMM for the per-byte segmented-sum products (fp32 operands: S holds sums of up
+// to B*T alpha-scaled gradients and may exceed the fp16 range).  part[z] = sum_k A(m, k) B(k, n)
+// over split z; 64 x 64 tile, 256 threads x (4 x 4) outputs, K staged 32 at a time.
+//   MODE 0 (dE):    A(m=v, k=r) = Scan[v][r],  B(k=r, n=c) = [W_mx; W_x]_canonical[r][c]
+//   MODE 1 (dWcat): A(m=r, k=v) = Scan[v][r],  B(k=v, n=c) = E[v][c]
+template <typename S, int MODE>
+__global__ void __launch_bounds__(256) seg_gemm_kernel(Net<S> n, float* __restrict__ part, int M, int N, int K,
+                                                       int k_per_split) {
+  __shared__ float As[32][64 + 4];
+  __shared__ float Bs[32][64 + 4];
+  const int h = n.h, e = n.e, R = 5 * h;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int kbeg = blockIdx.z * k_per_split, kend = min(K, kbeg + k_per_split);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[4][4] = {};
+  for (int k0 = kbeg; k0 < kend; k0 += 32) {
+    for (int i = threadIdx.x; i < 32 * 64; i += 256) {
+      int kk, mm;
+      if (MODE == 0) { mm = i >> 5; kk = i & 31; }   // Scan[v][r] with v = m: coalesce over k
+      else { kk = i >> 6; mm = i & 63; }             // Scan[v][r] with r = m: coalesce over m
+      const int gm = m0 + mm, gk = k0 + kk;
+      float a = 0.f;
+      if (gm < M && gk < kend) a = (MODE == 0) ? n.Scan[(long)gm * R + gk] : n.Scan[(long)gk * R + gm];
+      As[kk][mm] = a;
+    }
+    for (int i = threadIdx.x; i < 32 * 64; i += 256) {
+      const int kk = i >> 6, nn = i & 63, gk = k0 + kk, gn = n0 + nn;
+      float bv = 0.f;
+      if (gk < kend && gn < N) {
+        if (MODE == 0) {
+          const long wrow = (gk < h) ? gk : (long)h + int_row((gk - h) / h, (gk - h) % h);
+          bv = to_f(n.Wcat_w[wrow * e + gn]);
+        } else {
+          bv = to_f(n.E_w[(long)gk * e + gn]);
+        }
+      }
+      Bs[kk][nn] = bv;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk) {
+      float a[4], bb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bb[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float* dst = part + (long)blockIdx.z * M * N;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gm = m0 + ty * 4 + i, gn = n0 + tx * 4 + j;
+      if (gm < M && gn < N) dst[(long)gm * N + gn] = acc[i][j];
+    }
+}
+
+// Sums the split-K partials in order and stores dE (MODE 0) or [dW_mx; dW_x] (MODE 1) in the arena.
+template <typename S, int MODE>
+__global__ void seg_finalize_kernel(Net<S> n, const float* __restrict__ part, int splits, int M, int N) {
+  const long MN = (long)M * N;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < MN; i += (long)gridDim.x * blockDim.x) {
     float s = 0.f;
-    for (int v = 0; v < 256; ++v) s += n.Scan[(long)v * 5 * h + r] * to_f(n.E_w[(long)v * e + c]);
-    const long dst = (r < h) ? n.po.Wmx + (long)r * e + c : n.po.Wx + (long)(r - h) * e + c;
+    for (int z = 0; z < splits; ++z) s += part[z * MN + i];
+    const int r = (int)(i / N), c = (int)(i % N);
+    long dst;
+    if (MODE == 0) dst = n.po.E + i;
+    else dst = (r < n.h) ? n.po.Wmx + (long)r * n.e + c : n.po.Wx + (long)(r - n.h) * n.e + c;
     n.arena[dst] = to_s<S>(s);
   }
 }
 
-// dE[v] = sum_r S[v][r] [W_mx; W_x][r]  (the embedding gradient, segmented by byte), and
 // db = sum_v S_x[v].
-template <typename S>
-__global__ void __launch_bounds__(256) de_kernel(Net<S> n) {
-  __shared__ float red[4][64];
-  const int h = n.h, e = n.e, v = blockIdx.x;
-  const int grp = threadIdx.x >> 6, cl = threadIdx.x & 63;
-  const int R = 5 * h, per = (R + 3) / 4;
-  for (int c0 = 0; c0 < e; c0 += 64) {
-    const int c = c0 + cl;
-    float s = 0.f;
-    if (c < e) {
-      const int rb = grp * per, re = min(R, rb + per);
-      for (int r = rb; r < re; ++r) {
-        const long wrow = (r < h) ? r : (long)h + int_row((r - h) / h, (r - h) % h);
-        s += n.Scan[(long)v * R + r] * to_f(n.Wcat_w[wrow * e + c]);
-      }
-    }
-    red[grp][cl] = s;
-    __syncthreads();
-    if (grp == 0 && c < e) n.arena[n.po.E + (long)v * e + c] = to_s<S>(((red[0][cl] + red[1][cl]) + red[2][cl]) + red[3][cl]);
-    __syncthreads();
-  }
-}
-
 template <typename S>
 __global__ void db_kernel(Net<S> n) {
   const int h = n.h;
@@ -369,6 +409,24 @@ __global__ void overflow_kernel(const S* __restrict__ buf, long count, int32_t* 
 
 // Unscale + Adam on fp32 masters + fp16 working-copy cast; a no-op when the step overflowed.
 template <typename S>
+__device__ __forceinline__ void load4(const S* p, float* g);
+template <>
+__device__ __forceinline__ void load4<__half>(const __half* p, float* g) {
+  const uint2 w = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
+  g[0] = a.x; g[1] = a.y; g[2] = b.x; g[3] = b.y;
+}
+template <>
+__device__ __forceinline__ void load4<float>(const float* p, float* g) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  g[0] = v.x; g[1] = v.y; g[2] = v.z; g[3] = v.w;
+}
+
+// Unscale + Adam on fp32 masters + fp16 working-copy cast, 4 consecutive parameters per thread
+// (P, e, h are multiples of 64, so a group never straddles a tensor or a row); a no-op when the
+// step overflowed.
+template <typename S>
 __global__ void adam_kernel(Net<S> n, float* __restrict__ m, float* __restrict__ v, float beta1, float beta2,
                             float eps, double lr0, long decay) {
   const DevState* st = n.st;
@@ -379,15 +437,29 @@ __global__ void adam_kernel(Net<S> n, float* __restrict__ m, float* __restrict__
   const float bc1 = (float)(1.0 - pow((double)beta1, (double)tau));
   const float bc2 = (float)(1.0 - pow((double)beta2, (double)tau));
   const float lrf = (float)lr;
-  for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n.po.P; q += (long)gridDim.x * blockDim.x) {
-    const float g = to_f(n.arena[q]) * inv_alpha;
-    const float mm = beta1 * m[q] + (1.f - beta1) * g;
-    const float vv = beta2 * v[q] + (1.f - beta2) * g * g;
-    const float th = n.master[q] - lrf * (mm / bc1) / (sqrtf(vv / bc2) + eps);
-    m[q] = mm;
-    v[q] = vv;
-    n.master[q] = th;
-    store_working(n, q, th);
+  const long P4 = n.po.P / 4;
+  for (long q4 = blockIdx.x * (long)blockDim.x + threadIdx.x; q4 < P4; q4 += (long)gridDim.x * blockDim.x) {
+    const long q = q4 * 4;
+    float g[4];
+    load4<S>(n.arena + q, g);
+    float4 mm = reinterpret_cast<const float4*>(m)[q4];
+    float4 vv = reinterpret_cast<const float4*>(v)[q4];
+    float4 th = reinterpret_cast<const float4*>(n.master)[q4];
+    float* mp = &mm.x;
+    float* vp = &vv.x;
+    float* tp = &th.x;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float gi = g[i] * inv_alpha;
+      mp[i] = beta1 * mp[i] + (1.f - beta1) * gi;
+      vp[i] = beta2 * vp[i] + (1.f - beta2) * gi * gi;
+      tp[i] = tp[i] - lrf * (mp[i] / bc1) / (sqrtf(vp[i] / bc2) + eps);
+    }
+    reinterpret_cast<float4*>(m)[q4] = mm;
+    reinterpret_cast<float4*>(v)[q4] = vv;
+    reinterpret_cast<float4*>(n.master)[q4] = th;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) store_working(n, q + i, tp[i]);
   }
 }
 

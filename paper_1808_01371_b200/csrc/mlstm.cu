@@ -37,6 +37,7 @@ struct Opd {  // K-major operand view: [zdim][rows][K], element strides ld (row)
 
 struct Plan {
   int bn, splits;
+  bool pair;  // CTA-pair (cta_group::2) 256-row tiles
 };
 
 long rup(long x, long m) { return (x + m - 1) / m * m; }
@@ -63,6 +64,7 @@ struct mlstm_ctx {
   DevState* st_host = nullptr;  // pinned
   int nblk_ce = 0;
   long part_elems = 0;
+  int seg_splits = 1;
   Net<__half> nh{};
   Net<float> nf{};
   ncclComm_t comm = nullptr;
@@ -128,8 +130,21 @@ int grid_for(long n, int threads = 256, int cap = 148 * 16) {
 }
 
 // Tile-N and split-K choice shared by the workspace layout and the launches.
+// Engine choice (measured with mlstm_gemm_bench, profiles/r01_gemm_sweep.log): tcgen05 issue
+// rate per k-block is nearly flat in N, so wide (BN = 256) tiles matter most; the CTA-pair engine
+// (256 x 256 per pair) halves per-SM operand traffic and wins whenever it can fill ~60 pairs,
+// with split-K where allowed.  Otherwise one CTA per 128-row tile with the widest BN that still
+// fills ~120 SMs.
 Plan plan_gemm(bool tc, long M, long N, long K, bool allow_split) {
-  Plan p{64, 1};
+  Plan p{64, 1, false};
+  const long kb = (K + 63) / 64;
+  if (tc && M > 128) {
+    const long pairs = ((M + 255) / 256) * ((N + 255) / 256);
+    int sp = 1;
+    if (allow_split)
+      while (pairs * sp < 60 && kb / (sp * 2) >= 8) sp *= 2;
+    if (pairs * sp >= 60) return Plan{256, sp, true};
+  }
   const long mt = (M + 127) / 128;
   if (tc) {
     for (int bn : {256, 128, 64}) {
@@ -141,7 +156,6 @@ Plan plan_gemm(bool tc, long M, long N, long K, bool allow_split) {
   }
   if (allow_split) {
     const long tiles = mt * ((N + p.bn - 1) / p.bn);
-    const long kb = (K + 63) / 64;
     while (tiles * p.splits < 148 && kb / (p.splits * 2) >= 4) p.splits *= 2;
   }
   return p;
@@ -196,6 +210,9 @@ void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
     Plan p = plan_gemm(c->tc, s[0], s[1], K, true);
     if (p.splits > 1) part = std::max(part, (long)p.splits * s[0] * s[1]);
   }
+  c->seg_splits = (int)std::max(1L, std::min(64L, (5L * h) / 512));
+  part = std::max(part, (long)c->seg_splits * 256 * e);
+  part = std::max(part, 5L * h * e);
   c->part_elems = part;
   n.part = cv.take<float>(part);
   n.Scan = cv.take<float>(256L * 5 * h);
@@ -312,6 +329,21 @@ cudaError_t launch_tc(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb
   return cudaGetLastError();
 }
 
+template <int BN, class Epi>
+cudaError_t launch_tc2(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az,
+                       int bz, int splits, const Epi& epi) {
+  auto kern = gemm_tc2_kernel<BN, Epi>;
+  const int smem = Tc2Cfg<BN>::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int kb = (K + 63) / 64;
+  const int kbps = (kb + splits - 1) / splits;
+  dim3 grid(2 * ((N + BN - 1) / BN), (M + 255) / 256, splits);
+  kern<<<grid, 192, smem, c->stream>>>(*ma, *mb, M, N, K, az, bz, kbps, epi);
+  count_launch(c);
+  return cudaGetLastError();
+}
+
 // D[M x N] = A[az] . B[bz]^T, fused epilogue.  `splits` > 1 only with a partial epilogue.
 template <typename S, class Epi>
 mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int M, int N, int K, Plan p,
@@ -319,16 +351,24 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
   if constexpr (std::is_same<S, __half>::value) {
     if (c->tc) {
     const CUtensorMap* ma = get_map(c, A, 128);
-    const CUtensorMap* mb = get_map(c, B, p.bn);
+    const CUtensorMap* mb = get_map(c, B, p.pair ? p.bn / 2 : p.bn);
     if (!ma || !mb) {
       c->failed = MLSTM_ECUDA;
       return MLSTM_ECUDA;
     }
     cudaError_t e;
-    switch (p.bn) {
-      case 256: e = launch_tc<256>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
-      case 128: e = launch_tc<128>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
-      default: e = launch_tc<64>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
+    if (p.pair) {
+      switch (p.bn) {
+        case 256: e = launch_tc2<256>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
+        case 128: e = launch_tc2<128>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
+        default: e = launch_tc2<64>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
+      }
+    } else {
+      switch (p.bn) {
+        case 256: e = launch_tc<256>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
+        case 128: e = launch_tc<128>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
+        default: e = launch_tc<64>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
+      }
     }
     CUDA_OR_FAIL(c, e);
     return MLSTM_OK;
@@ -486,8 +526,17 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
                                                                                           (int)w.N, w.off, w.mode)));
       }
     }
-    LAUNCH(c, (dwcat_kernel<S><<<(5 * h + 3) / 4, dim3(64, 4), 0, c->stream>>>(n)));
-    LAUNCH(c, (de_kernel<S><<<256, 256, 0, c->stream>>>(n)));
+    // dE = S [W_mx; W_x] (M=256, N=e, K=5h) and [dW_mx; dW_x] = S^T E (M=5h, N=e, K=256)
+    {
+      const int sp = c->seg_splits;
+      const int kps = (int)rup((5L * h + sp - 1) / sp, 32);
+      LAUNCH(c, (seg_gemm_kernel<S, 0><<<dim3((c->e + 63) / 64, 4, sp), 256, 0, c->stream>>>(n, n.part, 256, c->e,
+                                                                                               5 * h, kps)));
+      LAUNCH(c, (seg_finalize_kernel<S, 0><<<grid_for(256L * c->e), 256, 0, c->stream>>>(n, n.part, sp, 256, c->e)));
+      LAUNCH(c, (seg_gemm_kernel<S, 1><<<dim3((c->e + 63) / 64, (5 * h + 63) / 64, 1), 256, 0, c->stream>>>(
+                     n, n.part, 5 * h, c->e, 256, 256)));
+      LAUNCH(c, (seg_finalize_kernel<S, 1><<<grid_for(5L * h * c->e), 256, 0, c->stream>>>(n, n.part, 1, 5 * h, c->e)));
+    }
     LAUNCH(c, (db_kernel<S><<<grid_for(4L * h), 256, 0, c->stream>>>(n)));
   }
   return MLSTM_OK;
@@ -1028,6 +1077,53 @@ int32_t mlstm_launches_per_step(mlstm_ctx* c) {
     if (s != MLSTM_OK) return -1;
   }
   return c->launches;
+}
+
+mlstm_status mlstm_gemm_bench(int engine, int M, int N, int K, int bn, int iters, double* ms) {
+  if (!ms || M <= 0 || N <= 0 || K <= 0 || iters <= 0 || (engine != 1 && engine != 2) ||
+      (bn != 0 && bn != 64 && bn != 128 && bn != 256) || N % 64 || K % 8)
+    return fail(MLSTM_EINVAL, "bad gemm_bench arguments");
+  if (!get_encoder()) return fail(MLSTM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  mlstm_ctx c;
+  c.tc = true;
+  __half *A = nullptr, *B = nullptr;
+  float* D = nullptr;
+  cudaEvent_t e0, e1;
+  auto cleanup = [&]() {
+    cudaFree(A);
+    cudaFree(B);
+    cudaFree(D);
+  };
+  if (cudaMalloc(&A, 2L * M * K) != cudaSuccess || cudaMalloc(&B, 2L * N * K) != cudaSuccess ||
+      cudaMalloc(&D, 4L * M * N) != cudaSuccess) {
+    cleanup();
+    return fail(MLSTM_ECUDA, "cudaMalloc");
+  }
+  const long nA = (long)M * K, nB = (long)N * K;
+  cudaMemset(A, 0x3c, 2L * M * K);  // operand values do not matter for timing
+  cudaMemset(B, 0x3c, 2L * N * K);
+  Opd oa{A, M, K, K, 1, nA}, ob{B, N, K, K, 1, nB};
+  Plan p = plan_gemm(true, M, N, K, false);
+  p.pair = engine == 2;
+  if (bn) p.bn = bn;
+  EpiPartial epi{D, N, (long)M * N};
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  mlstm_status st = gemm<__half>(&c, oa, 0, ob, 0, M, N, K, p, epi);
+  if (st == MLSTM_OK) {
+    cudaEventRecord(e0);
+    for (int i = 0; i < iters && st == MLSTM_OK; ++i) st = gemm<__half>(&c, oa, 0, ob, 0, M, N, K, p, epi);
+    cudaEventRecord(e1);
+    cudaError_t e = cudaEventSynchronize(e1);
+    float t = 0;
+    cudaEventElapsedTime(&t, e0, e1);
+    *ms = t / iters;
+    if (e != cudaSuccess) st = fail(MLSTM_ECUDA, cudaGetErrorString(e));
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cleanup();
+  return st;
 }
 
 const char* mlstm_last_error(void) { return g_err.c_str(); }

@@ -88,6 +88,8 @@ _SIGS = {
     "mlstm_phase_times": (ctypes.c_int, [_vp, _dp, _i32p, _i32p]),
     "mlstm_phase_name": (ctypes.c_char_p, [ctypes.c_int]),
     "mlstm_launches_per_step": (ctypes.c_int32, [_vp]),
+    "mlstm_gemm_bench": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, _dp]),
     "mlstm_last_error": (ctypes.c_char_p, []),
     "mlstm_destroy": (None, [_vp]),
 }
@@ -198,6 +200,12 @@ def mlstm_scale_lr(base_lr: float, rule: int, batch: int, ref_batch: int = 128) 
 
 def mlstm_bpc_from_nats(nats: float) -> float:
     return lib().mlstm_bpc_from_nats(nats)
+
+
+def mlstm_gemm_bench(engine: int, M: int, N: int, K: int, bn: int = 0, iters: int = 20) -> float:
+    ms = ctypes.c_double()
+    _check(lib().mlstm_gemm_bench(engine, M, N, K, bn, iters, ctypes.byref(ms)))
+    return ms.value
 
 
 def mlstm_destroy(ctx):
