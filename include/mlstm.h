@@ -177,7 +177,8 @@ int32_t mlstm_launches_per_step(mlstm_ctx* ctx);
 
 /* Diagnostics: times `iters` launches of the tensor-core GEMM engine on random fp16 operands
  * D[M x N] = A[M x K] B[N x K]^T (fp32 out), engine 1 = one CTA per 128-row tile, 2 = CTA pair
- * (cta_group::2) per 256-row tile; bn = tile N (64/128/256; 0 = the library's choice).  Allocates
+ * (cta_group::2) per 256-row tile, 3 = the library's own plan for the shape (CTA pairs with the
+ * K loop split over a cluster when needed); bn = tile N (64/128/256; 0 = library's choice).  Allocates
  * and frees its own device buffers.  *ms = average device time per launch (CUDA events). */
 mlstm_status mlstm_gemm_bench(int engine, int M, int N, int K, int bn, int iters, double* ms);
 

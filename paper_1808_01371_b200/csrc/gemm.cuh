@@ -266,6 +266,313 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// gemm_tc2s_kernel: CTA-pair 256 x 256 tiles with the K loop split S ways across S pairs of one
+// cluster (2S CTAs; cluster rank r: row half r & 1, K-split r >> 1).  Used where the output is too
+// small to fill the machine with 256-wide tiles (the per-timestep GEMMs with N = h).  After the
+// mainloop every CTA stages its fp32 partial in its own (now idle) pipeline shared memory; after a
+// cluster barrier, CTA r reduces columns [z*256/S, (z+1)*256/S) of its 128 rows over the S
+// partials through DSMEM in fixed order z = 0..S-1 (deterministic) and runs the fused epilogue on
+// that slice -- so the epilogue work stays spread over all 2S CTAs.
+template <int S, class Epi>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tc2s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                     int N, int K, int az, int bz, int kb_per_split, Epi epi) {
+  constexpr int BN = 256;
+  using C = Tc2Cfg<BN>;
+  constexpr int SLICE = BN / S;
+  constexpr int LDS = BN + 4;  // staging row stride in floats (odd number of 16-byte units)
+  static_assert(128 * LDS * 4 <= C::STAGES * C::STAGE_BYTES, "staging must fit in the pipeline smem");
+  static_assert(SLICE % 64 == 0, "slice is a whole number of epilogue chunks");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  float* stage = reinterpret_cast<float*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* accf = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const uint32_t half = rank & 1u, z = rank >> 1, pair_leader = rank & ~1u;
+  const bool leader = half == 0;
+  const int n0 = (blockIdx.x / (2 * S)) * BN;
+  const int m0 = blockIdx.y * 256 + half * 128;
+  const int total_kb = (K + C::BK - 1) / C::BK;
+  const int kb0 = z * kb_per_split;
+  const int nkb = max(0, min(kb_per_split, total_kb - kb0));
+
+  if (threadIdx.x == 0) {
+#pragma unroll 1
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::mbar_init(accf, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc2(tmem_slot, BN);
+    ptx::tmem_relinquish2();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && nkb > 0) {
+      const uint64_t pol = ptx::policy_evict_last();
+      const uint32_t full_leader0 = ptx::mapa_shared(ptx::smem_u32(&full[0]), pair_leader);
+#pragma unroll 1
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % C::STAGES;
+        const uint32_t ph = (i / C::STAGES) & 1;
+        ptx::mbar_wait(&empty[s], ph ^ 1);
+        if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * C::STAGE_BYTES);
+        const int kc = (kb0 + i) * C::BK;
+        ptx::tma_load_3d_2sm(sA + s * C::A_BYTES, &tmA, full_leader0 + s * 8, kc, m0, az, pol);
+        ptx::tma_load_3d_2sm(sB + s * C::B_BYTES, &tmB, full_leader0 + s * 8, kc, n0 + half * (BN / 2), bz, pol);
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0 && nkb > 0) {
+      constexpr uint32_t idesc = ptx::idesc_f16_f32(256, BN);
+      const uint16_t mask = static_cast<uint16_t>(3u << pair_leader);
+#pragma unroll 1
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % C::STAGES;
+        const uint32_t ph = (i / C::STAGES) & 1;
+        ptx::mbar_wait(&full[s], ph);
+        ptx::tc_fence_after();
+        const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
+        const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
+#pragma unroll
+        for (int k = 0; k < C::BK / 16; ++k)
+          ptx::mma_f16_2sm(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
+        ptx::mma_commit_2sm_mc(&empty[s], mask);
+      }
+      ptx::mma_commit_2sm_mc(accf, mask);
+    }
+  } else {
+    // stage this CTA's fp32 partial (128 rows x 256 cols) in its own shared memory
+    const int q = warp & 3;
+    const int rl = q * 32 + lane;
+    if (nkb > 0) {
+      ptx::mbar_wait(accf, 0);
+      ptx::tc_fence_after();
+    }
+#pragma unroll 1
+    for (int c = 0; c < BN / 64; ++c) {
+      float v[64];
+      if (nkb > 0) {
+        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 64;
+        ptx::tmem_ld16(ta, v);
+        ptx::tmem_ld16(ta + 16, v + 16);
+        ptx::tmem_ld16(ta + 32, v + 32);
+        ptx::tmem_ld16(ta + 48, v + 48);
+        ptx::tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) v[i] = 0.f;
+      }
+      float4* dst = reinterpret_cast<float4*>(stage + rl * LDS + c * 64);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();  // every partial of the cluster is staged
+  if (warp >= 2) {
+    const int q = warp & 3;
+    const int rl = q * 32 + lane;
+    const int row = m0 + rl;
+    const uint32_t my = ptx::smem_u32(stage + rl * LDS + z * SLICE);
+#pragma unroll 1
+    for (int j = 0; j < SLICE / 64; ++j) {
+      float v[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = 0.f;
+#pragma unroll 1
+      for (int zz = 0; zz < S; ++zz) {
+        const uint32_t src = ptx::mapa_shared(my, 2 * zz + half) + j * 256;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float4 p = ptx::ld_dsmem_f4(src + 16 * i);
+          v[4 * i] += p.x;
+          v[4 * i + 1] += p.y;
+          v[4 * i + 2] += p.z;
+          v[4 * i + 3] += p.w;
+        }
+      }
+      const int col0 = n0 + z * SLICE + j * 64;
+      if (row < M && col0 < N) epi(row, col0, v);
+    }
+  }
+  ptx::cluster_sync();  // no CTA leaves while others still read its staging buffer
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc2(tmem, BN);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// gemm_tc1s_kernel: one CTA per 128 x 256 tile (full-rate M=128, N=256 tcgen05.mma) with the K
+// loop split S ways over the S CTAs of a cluster (cluster rank z = K split).  Used when 256-wide
+// tiles alone cannot fill the machine (the per-timestep GEMMs with N = h).  Each CTA writes its
+// fp32 partial to an L2-resident scratch; after the cluster barrier (release/acquire at cluster
+// scope orders those writes) CTA z sums columns [z*256/S, (z+1)*256/S) of its 128 rows over the S
+// partials in fixed order z' = 0..S-1 (deterministic) and runs the fused epilogue on that slice,
+// so the epilogue work stays spread over all S CTAs of the tile.
+template <int S, class Epi>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tc1s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                     int N, int K, int az, int bz, int kb_per_split, float* __restrict__ scratch, Epi epi) {
+  constexpr int BN = 256;
+  using C = TcCfg<BN>;
+  constexpr int SLICE = BN / S;
+  static_assert(SLICE % 64 == 0, "slice is a whole number of epilogue chunks");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* accf = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int z = (int)ptx::cluster_ctarank();
+  const int tile_n = blockIdx.x / S;
+  const int n0 = tile_n * BN, m0 = blockIdx.y * C::BM;
+  const int total_kb = (K + C::BK - 1) / C::BK;
+  const int kb0 = z * kb_per_split;
+  const int nkb = max(0, min(kb_per_split, total_kb - kb0));
+  // this tile's S partials: scratch[(tile * S + z')][128][256]
+  float* part = scratch + ((long)(blockIdx.y * (gridDim.x / S) + tile_n) * S) * (128L * BN);
+
+  if (threadIdx.x == 0) {
+#pragma unroll 1
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::mbar_init(accf, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc(tmem_slot, BN);
+    ptx::tmem_relinquish();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && nkb > 0) {
+      const uint64_t pol = ptx::policy_evict_last();
+#pragma unroll 1
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % C::STAGES;
+        const uint32_t ph = (i / C::STAGES) & 1;
+        ptx::mbar_wait(&empty[s], ph ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+        const int kc = (kb0 + i) * C::BK;
+        ptx::tma_load_3d(sA + s * C::A_BYTES, &tmA, &full[s], kc, m0, az, pol);
+        ptx::tma_load_3d(sB + s * C::B_BYTES, &tmB, &full[s], kc, n0, bz, pol);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nkb > 0) {
+      constexpr uint32_t idesc = ptx::idesc_f16_f32(C::BM, BN);
+#pragma unroll 1
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % C::STAGES;
+        const uint32_t ph = (i / C::STAGES) & 1;
+        ptx::mbar_wait(&full[s], ph);
+        ptx::tc_fence_after();
+        const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
+        const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
+#pragma unroll
+        for (int k = 0; k < C::BK / 16; ++k)
+          ptx::mma_f16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
+        ptx::mma_commit(&empty[s]);
+      }
+      ptx::mma_commit(accf);
+    }
+  } else {
+    const int q = warp & 3;
+    const int rl = q * 32 + lane;
+    if (nkb > 0) {
+      ptx::mbar_wait(accf, 0);
+      ptx::tc_fence_after();
+    }
+    float4* dst = reinterpret_cast<float4*>(part + (long)z * 128 * BN + (long)rl * BN);
+#pragma unroll 1
+    for (int c = 0; c < BN / 64; ++c) {
+      float v[64];
+      if (nkb > 0) {
+        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 64;
+        ptx::tmem_ld16(ta, v);
+        ptx::tmem_ld16(ta + 16, v + 16);
+        ptx::tmem_ld16(ta + 32, v + 32);
+        ptx::tmem_ld16(ta + 48, v + 48);
+        ptx::tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) v[i] = 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) dst[c * 16 + i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();  // all S partials of the tile are written (cluster-scope release/acquire)
+  if (warp >= 2) {
+    const int q = warp & 3;
+    const int rl = q * 32 + lane;
+    const int row = m0 + rl;
+#pragma unroll 1
+    for (int j = 0; j < SLICE / 64; ++j) {
+      const int cl = z * SLICE + j * 64;
+      float v[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = 0.f;
+#pragma unroll 1
+      for (int zz = 0; zz < S; ++zz) {
+        const float4* src = reinterpret_cast<const float4*>(part + (long)zz * 128 * BN + (long)rl * BN + cl);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float4 p = __ldcg(src + i);
+          v[4 * i] += p.x;
+          v[4 * i + 1] += p.y;
+          v[4 * i + 2] += p.z;
+          v[4 * i + 3] += p.w;
+        }
+      }
+      const int col0 = n0 + cl;
+      if (row < M && col0 < N) epi(row, col0, v);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, BN);
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ float ld_as_float(const T* p) {
   return static_cast<float>(*p);

@@ -37,8 +37,10 @@ struct Opd {  // K-major operand view: [zdim][rows][K], element strides ld (row)
 
 struct Plan {
   int bn, splits;
-  bool pair;  // CTA-pair (cta_group::2) 256-row tiles
+  bool pair;     // CTA-pair (cta_group::2) 256-row tiles
+  bool cluster;  // K split over the CTAs of a cluster, reduced in-kernel (1-CTA 128 x 256 tiles)
 };
+constexpr long kSplitScratchFloats = 160L * 128 * 256;  // >= tiles * S partials of any cluster-split plan
 
 long rup(long x, long m) { return (x + m - 1) / m * m; }
 
@@ -65,6 +67,7 @@ struct mlstm_ctx {
   int nblk_ce = 0;
   long part_elems = 0;
   int seg_splits = 1;
+  float* split_scratch = nullptr;
   Net<__half> nh{};
   Net<float> nf{};
   ncclComm_t comm = nullptr;
@@ -136,17 +139,17 @@ int grid_for(long n, int threads = 256, int cap = 148 * 16) {
 // with split-K where allowed.  Otherwise one CTA per 128-row tile with the widest BN that still
 // fills ~120 SMs.
 Plan plan_gemm(bool tc, long M, long N, long K, bool allow_split) {
-  Plan p{64, 1, false};
+  Plan p{64, 1, false, false};
   const long kb = (K + 63) / 64;
-  if (tc && M > 128) {
-    const long pairs = ((M + 255) / 256) * ((N + 255) / 256);
-    int sp = 1;
-    if (allow_split)
-      while (pairs * sp < 60 && kb / (sp * 2) >= 8) sp *= 2;
-    if (pairs * sp >= 60) return Plan{256, sp, true};
-  }
+  if (tc && M > 128 && ((M + 255) / 256) * ((N + 255) / 256) >= 60) return Plan{256, 1, true, false};
   const long mt = (M + 127) / 128;
   if (tc) {
+    // 128 x 256 tiles with the K loop split over a cluster of S <= 4 CTAs when 256-wide tiles
+    // alone cannot fill the GPU (measured: N=64 tiles issue MMAs at ~1/4 of the N=256 rate)
+    const long tiles = mt * ((N + 255) / 256);
+    int sp = 1;
+    while (tiles * sp < 100 && sp < 4 && kb / (sp * 2) >= 4) sp *= 2;
+    if (sp > 1 && tiles * sp <= 160) return Plan{256, sp, false, true};
     for (int bn : {256, 128, 64}) {
       if (mt * ((N + bn - 1) / bn) >= 120 || bn == 64) {
         p.bn = bn;
@@ -208,13 +211,14 @@ void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
   const long shapes[4][2] = {{4L * h, h}, {h, h}, {256, h}, {256, 5L * h}};
   for (auto& s : shapes) {
     Plan p = plan_gemm(c->tc, s[0], s[1], K, true);
-    if (p.splits > 1) part = std::max(part, (long)p.splits * s[0] * s[1]);
+    if (p.splits > 1 && !p.pair && !p.cluster) part = std::max(part, (long)p.splits * s[0] * s[1]);
   }
   c->seg_splits = (int)std::max(1L, std::min(64L, (5L * h) / 512));
   part = std::max(part, (long)c->seg_splits * 256 * e);
   part = std::max(part, 5L * h * e);
   c->part_elems = part;
   n.part = cv.take<float>(part);
+  c->split_scratch = c->tc ? cv.take<float>(kSplitScratchFloats) : nullptr;
   n.Scan = cv.take<float>(256L * 5 * h);
   n.hstate = cv.take<S>(2L * B * h);
   n.cstate = cv.take<float>(2L * B * h);
@@ -329,6 +333,58 @@ cudaError_t launch_tc(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb
   return cudaGetLastError();
 }
 
+template <int S, class Epi>
+cudaError_t launch_tc1s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az,
+                        int bz, const Epi& epi) {
+  auto kern = gemm_tc1s_kernel<S, Epi>;
+  const int smem = TcCfg<256>::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int kb = (K + 63) / 64;
+  const int kbps = (kb + S - 1) / S;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(S * ((N + 255) / 256), (M + 127) / 128, 1);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = S;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, *ma, *mb, M, N, K, az, bz, kbps, c->split_scratch, epi);
+  count_launch(c);
+  return e;
+}
+
+template <int S, class Epi>
+cudaError_t launch_tc2s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az,
+                        int bz, const Epi& epi) {
+  auto kern = gemm_tc2s_kernel<S, Epi>;
+  const int smem = Tc2Cfg<256>::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int kb = (K + 63) / 64;
+  const int kbps = (kb + S - 1) / S;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * S * ((N + 255) / 256), (M + 255) / 256, 1);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2 * S;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, *ma, *mb, M, N, K, az, bz, kbps, epi);
+  count_launch(c);
+  return e;
+}
+
 template <int BN, class Epi>
 cudaError_t launch_tc2(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az,
                        int bz, int splits, const Epi& epi) {
@@ -357,7 +413,13 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
       return MLSTM_ECUDA;
     }
     cudaError_t e;
-    if (p.pair) {
+    if (p.cluster) {
+      e = p.splits == 2 ? launch_tc1s<2>(c, ma, mb, M, N, K, az, bz, epi)
+                        : launch_tc1s<4>(c, ma, mb, M, N, K, az, bz, epi);
+    } else if (p.pair && p.splits > 1) {
+      e = p.splits == 2 ? launch_tc2s<2>(c, ma, mb, M, N, K, az, bz, epi)
+                        : launch_tc2s<4>(c, ma, mb, M, N, K, az, bz, epi);
+    } else if (p.pair) {
       switch (p.bn) {
         case 256: e = launch_tc2<256>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
         case 128: e = launch_tc2<128>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
@@ -518,7 +580,7 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
     };
     for (const W& w : ws) {
       const Plan p = plan_gemm(c->tc, w.M, w.N, Kt, true);
-      if (p.splits == 1) {
+      if (p.splits == 1 || p.pair || p.cluster) {
         RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kt, p, EpiWgrad<S>{n, w.off, w.mode, (int)w.N}));
       } else {
         RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kt, p, EpiPartial{n.part, w.N, w.M * w.N}));
@@ -1080,16 +1142,19 @@ int32_t mlstm_launches_per_step(mlstm_ctx* c) {
 }
 
 mlstm_status mlstm_gemm_bench(int engine, int M, int N, int K, int bn, int iters, double* ms) {
-  if (!ms || M <= 0 || N <= 0 || K <= 0 || iters <= 0 || (engine != 1 && engine != 2) ||
+  if (!ms || M <= 0 || N <= 0 || K <= 0 || iters <= 0 || engine < 1 || engine > 4 ||
       (bn != 0 && bn != 64 && bn != 128 && bn != 256) || N % 64 || K % 8)
     return fail(MLSTM_EINVAL, "bad gemm_bench arguments");
   if (!get_encoder()) return fail(MLSTM_ECUDA, "cuTensorMapEncodeTiled unavailable");
   mlstm_ctx c;
   c.tc = true;
+  if (cudaMalloc(&c.split_scratch, sizeof(float) * kSplitScratchFloats) != cudaSuccess)
+    return fail(MLSTM_ECUDA, "cudaMalloc");
   __half *A = nullptr, *B = nullptr;
   float* D = nullptr;
   cudaEvent_t e0, e1;
   auto cleanup = [&]() {
+    cudaFree(c.split_scratch);
     cudaFree(A);
     cudaFree(B);
     cudaFree(D);
@@ -1104,8 +1169,17 @@ mlstm_status mlstm_gemm_bench(int engine, int M, int N, int K, int bn, int iters
   cudaMemset(B, 0x3c, 2L * N * K);
   Opd oa{A, M, K, K, 1, nA}, ob{B, N, K, K, 1, nB};
   Plan p = plan_gemm(true, M, N, K, false);
-  p.pair = engine == 2;
-  if (bn) p.bn = bn;
+  if (engine == 4) {  // CTA pairs, K split 2 ways over a cluster of 4
+    p.pair = true;
+    p.cluster = false;
+    p.splits = 2;
+    p.bn = 256;
+  } else if (engine != 3) {
+    p.cluster = false;
+    p.pair = engine == 2;
+    p.splits = 1;
+    if (bn) p.bn = bn;
+  }
   EpiPartial epi{D, N, (long)M * N};
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
