@@ -16,6 +16,69 @@
 
 namespace mlstm {
 
+// ---- optional intra-kernel timeline (mlstm_trace_enable): one record per CTA,
+// {tag, cta, t_start, t_first_tma, t_first_full, t_acc_ready, t_reduced, t_end} in ns.
+struct TraceRec {
+  uint64_t v[8];
+};
+__device__ TraceRec* g_trace = nullptr;
+__device__ unsigned int g_trace_n = 0;
+__device__ unsigned int g_trace_cap = 0;
+struct Trace {
+  uint64_t t[6];
+  __device__ __forceinline__ void mark(int i) { t[i] = ptx::globaltimer(); }
+};
+__device__ __forceinline__ void trace_flush(const uint64_t* ts, int tag) {
+  TraceRec* tr = g_trace;
+  if (!tr) return;
+  const unsigned int i = atomicAdd(&g_trace_n, 1u);
+  if (i >= g_trace_cap) return;
+  TraceRec r;
+  r.v[0] = (uint64_t)tag;
+  r.v[1] = blockIdx.x + (uint64_t)gridDim.x * (blockIdx.y + (uint64_t)gridDim.y * blockIdx.z);
+  for (int k = 0; k < 6; ++k) r.v[2 + k] = ts[k];
+  tr[i] = r;
+}
+__device__ __forceinline__ void epi_bar_() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+template <class E, class = void>
+struct IsTile {  // epilogue with a cooperative tile() member (see epilogues.cuh)
+  static constexpr bool value = false;
+};
+template <class E>
+struct IsTile<E, decltype(void(E::kTile))> {
+  static constexpr bool value = E::kTile;
+};
+
+// Stages a 128 x (64*nchunk) fp32 accumulator tile from TMEM into shared memory (row stride ldt):
+// thread = TMEM lane = tile row.
+__device__ __forceinline__ void stage_tmem_rows(float* T, int ldt, uint32_t tmem, int q, int lane, int nchunk,
+                                                bool have) {
+  const int rl = q * 32 + lane;
+#pragma unroll 1
+  for (int c = 0; c < nchunk; ++c) {
+    float v[64];
+    if (have) {
+      const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 64;
+      ptx::tmem_ld16(ta, v);
+      ptx::tmem_ld16(ta + 16, v + 16);
+      ptx::tmem_ld16(ta + 32, v + 32);
+      ptx::tmem_ld16(ta + 48, v + 48);
+      ptx::tmem_ld_wait();
+    } else {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = 0.f;
+    }
+    float4* dst = reinterpret_cast<float4*>(T + rl * ldt + c * 64);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  }
+}
+
+template <class Epi>
+struct EpiTag {
+  static constexpr int value = 0;
+};
+
 template <int BN>
 struct TcCfg {
   static constexpr int BM = 128, BK = 64;
@@ -29,7 +92,7 @@ struct TcCfg {
 template <int BN, class Epi>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                   int N, int K, int az, int bz, int kb_per_split, Epi epi) {
+                   int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, Epi epi) {
   using C = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -39,6 +102,12 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* accf = empty + C::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  __shared__ uint64_t tr_ts[6];
+  const bool tracing = g_trace != nullptr;
+  if (tracing && threadIdx.x == 0) {
+    for (int k = 1; k < 6; ++k) tr_ts[k] = 0;
+    tr_ts[0] = ptx::globaltimer();
+  }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * C::BM, n0 = blockIdx.x * BN;
@@ -70,7 +139,7 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0 && nkb > 0) {
-      const uint64_t pol = ptx::policy_evict_last();
+      const uint64_t pa = ptx::make_policy(polA), pb = ptx::make_policy(polB);
 #pragma unroll 1
       for (int i = 0; i < nkb; ++i) {
         const int s = i % C::STAGES;
@@ -78,8 +147,9 @@ __global__ void __launch_bounds__(192, 1)
         ptx::mbar_wait(&empty[s], ph ^ 1);
         ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
         const int kc = (kb0 + i) * C::BK;
-        ptx::tma_load_3d(sA + s * C::A_BYTES, &tmA, &full[s], kc, m0, az, pol);
-        ptx::tma_load_3d(sB + s * C::B_BYTES, &tmB, &full[s], kc, n0, bz, pol);
+        if (tracing && i == 0) tr_ts[1] = ptx::globaltimer();
+        ptx::tma_load_3d(sA + s * C::A_BYTES, &tmA, &full[s], kc, m0, az, pa);
+        ptx::tma_load_3d(sB + s * C::B_BYTES, &tmB, &full[s], kc, n0, bz, pb);
       }
     }
   } else if (warp == 1) {
@@ -91,6 +161,7 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t ph = (i / C::STAGES) & 1;
         ptx::mbar_wait(&full[s], ph);
         ptx::tc_fence_after();
+        if (tracing && i == 0) tr_ts[2] = ptx::globaltimer();
         const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
         const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
 #pragma unroll
@@ -107,6 +178,18 @@ __global__ void __launch_bounds__(192, 1)
       ptx::mbar_wait(accf, 0);
       ptx::tc_fence_after();
     }
+    if (tracing && threadIdx.x == 64) tr_ts[3] = ptx::globaltimer();
+    if constexpr (IsTile<Epi>::value) {
+      float* T = reinterpret_cast<float*>(smem);  // the pipeline stages are idle now
+      constexpr int ldt = BN + 4;
+      stage_tmem_rows(T, ldt, tmem, q, lane, BN / 64, nkb > 0);
+      ptx::tc_fence_before();
+      epi_bar_();
+      const int rows = min(128, M - (row - q * 32 - lane));
+      if (rows > 0 && n0 < N)
+        epi.tile(T, ldt, row - q * 32 - lane, n0, min(BN, N - n0), rows,
+                 reinterpret_cast<uint8_t*>(T + 128 * ldt), (int)threadIdx.x - 64);
+    } else {
 #pragma unroll 1
     for (int c = 0; c < BN / 64; ++c) {
       float v[64];
@@ -124,9 +207,14 @@ __global__ void __launch_bounds__(192, 1)
       const int col0 = n0 + c * 64;
       if (row < M && col0 < N) epi(row, col0, v);
     }
+    }
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (tracing && threadIdx.x == 0) {
+    tr_ts[5] = ptx::globaltimer();
+    trace_flush(tr_ts, EpiTag<Epi>::value);
+  }
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, BN);
@@ -154,7 +242,7 @@ struct Tc2Cfg {
 template <int BN, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                    int N, int K, int az, int bz, int kb_per_split, Epi epi) {
+                    int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, Epi epi) {
   using C = Tc2Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -164,6 +252,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* accf = empty + C::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  __shared__ uint64_t tr_ts[6];
+  const bool tracing = g_trace != nullptr;
+  if (tracing && threadIdx.x == 0) {
+    for (int k = 1; k < 6; ++k) tr_ts[k] = 0;
+    tr_ts[0] = ptx::globaltimer();
+  }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -198,7 +292,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0 && nkb > 0) {
-      const uint64_t pol = ptx::policy_evict_last();
+      const uint64_t pa = ptx::make_policy(polA), pb = ptx::make_policy(polB);
       const uint32_t full_leader0 = ptx::mapa_shared(ptx::smem_u32(&full[0]), 0);
 #pragma unroll 1
       for (int i = 0; i < nkb; ++i) {
@@ -211,8 +305,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         // by the same commit).  A release.cluster remote arrive here would fence every prior TMA.
         if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * C::STAGE_BYTES);
         const int kc = (kb0 + i) * C::BK;
-        ptx::tma_load_3d_2sm(sA + s * C::A_BYTES, &tmA, full_leader0 + s * 8, kc, m0, az, pol);
-        ptx::tma_load_3d_2sm(sB + s * C::B_BYTES, &tmB, full_leader0 + s * 8, kc, n0 + rank * (BN / 2), bz, pol);
+        if (tracing && i == 0) tr_ts[1] = ptx::globaltimer();
+        ptx::tma_load_3d_2sm(sA + s * C::A_BYTES, &tmA, full_leader0 + s * 8, kc, m0, az, pa);
+        ptx::tma_load_3d_2sm(sB + s * C::B_BYTES, &tmB, full_leader0 + s * 8, kc, n0 + rank * (BN / 2), bz, pb);
       }
     }
   } else if (warp == 1) {
@@ -224,6 +319,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         const uint32_t ph = (i / C::STAGES) & 1;
         ptx::mbar_wait(&full[s], ph);
         ptx::tc_fence_after();
+        if (tracing && i == 0) tr_ts[2] = ptx::globaltimer();
         const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
         const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
 #pragma unroll
@@ -240,6 +336,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       ptx::mbar_wait(accf, 0);
       ptx::tc_fence_after();
     }
+    if (tracing && threadIdx.x == 64) tr_ts[3] = ptx::globaltimer();
+    if constexpr (IsTile<Epi>::value) {
+      float* T = reinterpret_cast<float*>(smem);  // the pipeline stages are idle now
+      constexpr int ldt = BN + 4;
+      stage_tmem_rows(T, ldt, tmem, q, lane, BN / 64, nkb > 0);
+      ptx::tc_fence_before();
+      epi_bar_();
+      const int rows = min(128, M - (row - q * 32 - lane));
+      if (rows > 0 && n0 < N)
+        epi.tile(T, ldt, row - q * 32 - lane, n0, min(BN, N - n0), rows,
+                 reinterpret_cast<uint8_t*>(T + 128 * ldt), (int)threadIdx.x - 64);
+    } else {
 #pragma unroll 1
     for (int c = 0; c < BN / 64; ++c) {
       float v[64];
@@ -257,9 +365,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       const int col0 = n0 + c * 64;
       if (row < M && col0 < N) epi(row, col0, v);
     }
+    }
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();
+  if (tracing && threadIdx.x == 0) {
+    tr_ts[5] = ptx::globaltimer();
+    trace_flush(tr_ts, EpiTag<Epi>::value);
+  }
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc2(tmem, BN);
@@ -277,7 +390,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 template <int S, class Epi>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc2s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                     int N, int K, int az, int bz, int kb_per_split, Epi epi) {
+                     int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, Epi epi) {
   constexpr int BN = 256;
   using C = Tc2Cfg<BN>;
   constexpr int SLICE = BN / S;
@@ -293,6 +406,12 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* accf = empty + C::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  __shared__ uint64_t tr_ts[6];
+  const bool tracing = g_trace != nullptr;
+  if (tracing && threadIdx.x == 0) {
+    for (int k = 1; k < 6; ++k) tr_ts[k] = 0;
+    tr_ts[0] = ptx::globaltimer();
+  }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -328,7 +447,7 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0 && nkb > 0) {
-      const uint64_t pol = ptx::policy_evict_last();
+      const uint64_t pa = ptx::make_policy(polA), pb = ptx::make_policy(polB);
       const uint32_t full_leader0 = ptx::mapa_shared(ptx::smem_u32(&full[0]), pair_leader);
 #pragma unroll 1
       for (int i = 0; i < nkb; ++i) {
@@ -337,8 +456,9 @@ __global__ void __launch_bounds__(192, 1)
         ptx::mbar_wait(&empty[s], ph ^ 1);
         if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * C::STAGE_BYTES);
         const int kc = (kb0 + i) * C::BK;
-        ptx::tma_load_3d_2sm(sA + s * C::A_BYTES, &tmA, full_leader0 + s * 8, kc, m0, az, pol);
-        ptx::tma_load_3d_2sm(sB + s * C::B_BYTES, &tmB, full_leader0 + s * 8, kc, n0 + half * (BN / 2), bz, pol);
+        if (tracing && i == 0) tr_ts[1] = ptx::globaltimer();
+        ptx::tma_load_3d_2sm(sA + s * C::A_BYTES, &tmA, full_leader0 + s * 8, kc, m0, az, pa);
+        ptx::tma_load_3d_2sm(sB + s * C::B_BYTES, &tmB, full_leader0 + s * 8, kc, n0 + half * (BN / 2), bz, pb);
       }
     }
   } else if (warp == 1) {
@@ -351,6 +471,7 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t ph = (i / C::STAGES) & 1;
         ptx::mbar_wait(&full[s], ph);
         ptx::tc_fence_after();
+        if (tracing && i == 0) tr_ts[2] = ptx::globaltimer();
         const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
         const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
 #pragma unroll
@@ -368,6 +489,7 @@ __global__ void __launch_bounds__(192, 1)
       ptx::mbar_wait(accf, 0);
       ptx::tc_fence_after();
     }
+    if (tracing && threadIdx.x == 64) tr_ts[3] = ptx::globaltimer();
 #pragma unroll 1
     for (int c = 0; c < BN / 64; ++c) {
       float v[64];
@@ -389,6 +511,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();  // every partial of the cluster is staged
+  if (tracing && threadIdx.x == 0) tr_ts[4] = ptx::globaltimer();
   if (warp >= 2) {
     const int q = warp & 3;
     const int rl = q * 32 + lane;
@@ -416,6 +539,10 @@ __global__ void __launch_bounds__(192, 1)
     }
   }
   ptx::cluster_sync();  // no CTA leaves while others still read its staging buffer
+  if (tracing && threadIdx.x == 0) {
+    tr_ts[5] = ptx::globaltimer();
+    trace_flush(tr_ts, EpiTag<Epi>::value);
+  }
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc2(tmem, BN);
@@ -433,7 +560,8 @@ __global__ void __launch_bounds__(192, 1)
 template <int S, class Epi>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc1s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                     int N, int K, int az, int bz, int kb_per_split, float* __restrict__ scratch, Epi epi) {
+                     int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB,
+                     float* __restrict__ scratch, Epi epi) {
   constexpr int BN = 256;
   using C = TcCfg<BN>;
   constexpr int SLICE = BN / S;
@@ -446,6 +574,12 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* accf = empty + C::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  __shared__ uint64_t tr_ts[6];
+  const bool tracing = g_trace != nullptr;
+  if (tracing && threadIdx.x == 0) {
+    for (int k = 1; k < 6; ++k) tr_ts[k] = 0;
+    tr_ts[0] = ptx::globaltimer();
+  }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int z = (int)ptx::cluster_ctarank();
@@ -454,6 +588,7 @@ __global__ void __launch_bounds__(192, 1)
   const int total_kb = (K + C::BK - 1) / C::BK;
   const int kb0 = z * kb_per_split;
   const int nkb = max(0, min(kb_per_split, total_kb - kb0));
+  float* stage_T = reinterpret_cast<float*>(smem);  // tile-epilogue staging (stages idle by then)
   // this tile's S partials: scratch[(tile * S + z')][128][256]
   float* part = scratch + ((long)(blockIdx.y * (gridDim.x / S) + tile_n) * S) * (128L * BN);
 
@@ -481,7 +616,7 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0 && nkb > 0) {
-      const uint64_t pol = ptx::policy_evict_last();
+      const uint64_t pa = ptx::make_policy(polA), pb = ptx::make_policy(polB);
 #pragma unroll 1
       for (int i = 0; i < nkb; ++i) {
         const int s = i % C::STAGES;
@@ -489,8 +624,9 @@ __global__ void __launch_bounds__(192, 1)
         ptx::mbar_wait(&empty[s], ph ^ 1);
         ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
         const int kc = (kb0 + i) * C::BK;
-        ptx::tma_load_3d(sA + s * C::A_BYTES, &tmA, &full[s], kc, m0, az, pol);
-        ptx::tma_load_3d(sB + s * C::B_BYTES, &tmB, &full[s], kc, n0, bz, pol);
+        if (tracing && i == 0) tr_ts[1] = ptx::globaltimer();
+        ptx::tma_load_3d(sA + s * C::A_BYTES, &tmA, &full[s], kc, m0, az, pa);
+        ptx::tma_load_3d(sB + s * C::B_BYTES, &tmB, &full[s], kc, n0, bz, pb);
       }
     }
   } else if (warp == 1) {
@@ -502,6 +638,7 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t ph = (i / C::STAGES) & 1;
         ptx::mbar_wait(&full[s], ph);
         ptx::tc_fence_after();
+        if (tracing && i == 0) tr_ts[2] = ptx::globaltimer();
         const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
         const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
 #pragma unroll
@@ -518,7 +655,10 @@ __global__ void __launch_bounds__(192, 1)
       ptx::mbar_wait(accf, 0);
       ptx::tc_fence_after();
     }
-    float4* dst = reinterpret_cast<float4*>(part + (long)z * 128 * BN + (long)rl * BN);
+    if (tracing && threadIdx.x == 64) tr_ts[3] = ptx::globaltimer();
+    // partial layout [z][float4 column group (64)][row (128)]: lanes (= rows) write consecutive
+    // 16-byte vectors, fully coalesced; the reducer reads with the same mapping
+    float4* dst = reinterpret_cast<float4*>(part + (long)z * 128 * BN) + rl;
 #pragma unroll 1
     for (int c = 0; c < BN / 64; ++c) {
       float v[64];
@@ -534,11 +674,12 @@ __global__ void __launch_bounds__(192, 1)
         for (int i = 0; i < 64; ++i) v[i] = 0.f;
       }
 #pragma unroll
-      for (int i = 0; i < 16; ++i) dst[c * 16 + i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      for (int i = 0; i < 16; ++i) dst[(c * 16 + i) * 128] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
     }
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();  // all S partials of the tile are written (cluster-scope release/acquire)
+  if (tracing && threadIdx.x == 0) tr_ts[4] = ptx::globaltimer();
   if (warp >= 2) {
     const int q = warp & 3;
     const int rl = q * 32 + lane;
@@ -551,10 +692,10 @@ __global__ void __launch_bounds__(192, 1)
       for (int i = 0; i < 64; ++i) v[i] = 0.f;
 #pragma unroll 1
       for (int zz = 0; zz < S; ++zz) {
-        const float4* src = reinterpret_cast<const float4*>(part + (long)zz * 128 * BN + (long)rl * BN + cl);
+        const float4* src = reinterpret_cast<const float4*>(part + (long)zz * 128 * BN) + (cl / 4) * 128 + rl;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float4 p = __ldcg(src + i);
+          const float4 p = __ldcg(src + i * 128);
           v[4 * i] += p.x;
           v[4 * i + 1] += p.y;
           v[4 * i + 2] += p.z;
@@ -562,11 +703,29 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       const int col0 = n0 + cl;
-      if (row < M && col0 < N) epi(row, col0, v);
+      if constexpr (IsTile<Epi>::value) {
+        float4* dst = reinterpret_cast<float4*>(stage_T + rl * (SLICE + 4) + j * 64);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      } else {
+        if (row < M && col0 < N) epi(row, col0, v);
+      }
+    }
+    if constexpr (IsTile<Epi>::value) {
+      epi_bar_();
+      const int rows = min(128, M - m0);
+      const int c0 = n0 + z * SLICE;
+      if (rows > 0 && c0 < N)
+        epi.tile(stage_T, SLICE + 4, m0, c0, min(SLICE, N - c0), rows,
+                 reinterpret_cast<uint8_t*>(stage_T + 128 * (SLICE + 4)), (int)threadIdx.x - 64);
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (tracing && threadIdx.x == 0) {
+    tr_ts[5] = ptx::globaltimer();
+    trace_flush(tr_ts, EpiTag<Epi>::value);
+  }
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, BN);
@@ -626,7 +785,19 @@ __global__ void __launch_bounds__(128)
     __syncthreads();
   }
   const int row = m0 + tid;
-  if (row < M && n0 < N) epi(row, n0, acc);
+  if constexpr (IsTile<Epi>::value) {
+    extern __shared__ float simt_dyn[];
+    float* T = simt_dyn;
+    float4* dst = reinterpret_cast<float4*>(T + tid * 68);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) dst[i] = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+    __syncthreads();
+    const int rows = min(128, M - m0);
+    if (rows > 0 && n0 < N)
+      epi.tile(T, 68, m0, n0, min(64, N - n0), rows, reinterpret_cast<uint8_t*>(T + 128 * 68), tid);
+  } else {
+    if (row < M && n0 < N) epi(row, n0, acc);
+  }
 }
 
 }  // namespace mlstm

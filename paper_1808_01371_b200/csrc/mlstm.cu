@@ -22,6 +22,18 @@
 
 using namespace mlstm;
 
+namespace mlstm {  // trace tags of the fused epilogues (mlstm_trace_read)
+template <typename S> struct EpiTag<EpiF1<S>> { static constexpr int value = 1; };
+template <typename S> struct EpiTag<EpiF2<S>> { static constexpr int value = 2; };
+template <typename S> struct EpiTag<EpiB1<S>> { static constexpr int value = 3; };
+template <typename S> struct EpiTag<EpiB2<S>> { static constexpr int value = 4; };
+template <typename S> struct EpiTag<EpiY<S>> { static constexpr int value = 5; };
+template <typename S> struct EpiTag<EpiDHdec<S>> { static constexpr int value = 6; };
+template <typename S> struct EpiTag<EpiTab<S>> { static constexpr int value = 7; };
+template <typename S> struct EpiTag<EpiWgrad<S>> { static constexpr int value = 8; };
+template <> struct EpiTag<EpiPartial> { static constexpr int value = 9; };
+}  // namespace mlstm
+
 namespace {
 
 thread_local std::string g_err;
@@ -33,7 +45,10 @@ const char* kPhaseNames[NPH] = {"prep", "tab", "fwd_rec", "decoder", "ce", "dhde
 struct Opd {  // K-major operand view: [zdim][rows][K], element strides ld (row) and zstride
   const void* ptr;
   long rows, K, ld, zdim, zstride;
+  uint32_t pol = 0;  // L2 policy code for its TMA loads (ptx::make_policy)
 };
+constexpr uint32_t kPolFirst = 1u << 8;
+inline uint32_t pol_last(float frac) { return (2u << 8) | (uint32_t)(frac * 255.f + 0.5f); }
 
 struct Plan {
   int bn, splits;
@@ -67,6 +82,7 @@ struct mlstm_ctx {
   int nblk_ce = 0;
   long part_elems = 0;
   int seg_splits = 1;
+  float l2_wmh = 0.f, l2_wh = 0.f;  // evict_last fractions of the recurrent weights
   float* split_scratch = nullptr;
   Net<__half> nh{};
   Net<float> nf{};
@@ -260,6 +276,8 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   c->po.set(c->h, c->e);
   c->P = c->po.P;
   c->mixed = cfg->precision == MLSTM_MIXED;
+  if (const char* v = getenv("MLSTM_L2_WMH")) c->l2_wmh = (float)atof(v);  // tuning knobs
+  if (const char* v = getenv("MLSTM_L2_WH")) c->l2_wh = (float)atof(v);
   const char* dbg = getenv("MLSTM_DEBUG_SIMT_GEMM");  // test instrument: mixed mode on the SIMT engine
   c->tc = c->mixed && !(dbg && dbg[0] == '1');
 }
@@ -319,7 +337,7 @@ void count_launch(mlstm_ctx* c) {
 }
 
 template <int BN, class Epi>
-cudaError_t launch_tc(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az, int bz,
+cudaError_t launch_tc(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az, int bz, uint32_t pa, uint32_t pb,
                       int splits, const Epi& epi) {
   auto kern = gemm_tc_kernel<BN, Epi>;
   const int smem = TcCfg<BN>::SMEM;
@@ -328,14 +346,14 @@ cudaError_t launch_tc(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb
   const int kb = (K + 63) / 64;
   const int kbps = (kb + splits - 1) / splits;
   dim3 grid((N + BN - 1) / BN, (M + 127) / 128, splits);
-  kern<<<grid, 192, smem, c->stream>>>(*ma, *mb, M, N, K, az, bz, kbps, epi);
+  kern<<<grid, 192, smem, c->stream>>>(*ma, *mb, M, N, K, az, bz, kbps, pa, pb, epi);
   count_launch(c);
   return cudaGetLastError();
 }
 
 template <int S, class Epi>
 cudaError_t launch_tc1s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az,
-                        int bz, const Epi& epi) {
+                        int bz, uint32_t pa, uint32_t pb, const Epi& epi) {
   auto kern = gemm_tc1s_kernel<S, Epi>;
   const int smem = TcCfg<256>::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -354,14 +372,14 @@ cudaError_t launch_tc1s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, *ma, *mb, M, N, K, az, bz, kbps, c->split_scratch, epi);
+  e = cudaLaunchKernelEx(&cfg, kern, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, c->split_scratch, epi);
   count_launch(c);
   return e;
 }
 
 template <int S, class Epi>
 cudaError_t launch_tc2s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az,
-                        int bz, const Epi& epi) {
+                        int bz, uint32_t pa, uint32_t pb, const Epi& epi) {
   auto kern = gemm_tc2s_kernel<S, Epi>;
   const int smem = Tc2Cfg<256>::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -380,14 +398,14 @@ cudaError_t launch_tc2s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, *ma, *mb, M, N, K, az, bz, kbps, epi);
+  e = cudaLaunchKernelEx(&cfg, kern, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, epi);
   count_launch(c);
   return e;
 }
 
 template <int BN, class Epi>
 cudaError_t launch_tc2(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az,
-                       int bz, int splits, const Epi& epi) {
+                       int bz, uint32_t pa, uint32_t pb, int splits, const Epi& epi) {
   auto kern = gemm_tc2_kernel<BN, Epi>;
   const int smem = Tc2Cfg<BN>::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -395,7 +413,7 @@ cudaError_t launch_tc2(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* m
   const int kb = (K + 63) / 64;
   const int kbps = (kb + splits - 1) / splits;
   dim3 grid(2 * ((N + BN - 1) / BN), (M + 255) / 256, splits);
-  kern<<<grid, 192, smem, c->stream>>>(*ma, *mb, M, N, K, az, bz, kbps, epi);
+  kern<<<grid, 192, smem, c->stream>>>(*ma, *mb, M, N, K, az, bz, kbps, pa, pb, epi);
   count_launch(c);
   return cudaGetLastError();
 }
@@ -414,22 +432,22 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
     }
     cudaError_t e;
     if (p.cluster) {
-      e = p.splits == 2 ? launch_tc1s<2>(c, ma, mb, M, N, K, az, bz, epi)
-                        : launch_tc1s<4>(c, ma, mb, M, N, K, az, bz, epi);
+      e = p.splits == 2 ? launch_tc1s<2>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, epi)
+                        : launch_tc1s<4>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, epi);
     } else if (p.pair && p.splits > 1) {
-      e = p.splits == 2 ? launch_tc2s<2>(c, ma, mb, M, N, K, az, bz, epi)
-                        : launch_tc2s<4>(c, ma, mb, M, N, K, az, bz, epi);
+      e = p.splits == 2 ? launch_tc2s<2>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, epi)
+                        : launch_tc2s<4>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, epi);
     } else if (p.pair) {
       switch (p.bn) {
-        case 256: e = launch_tc2<256>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
-        case 128: e = launch_tc2<128>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
-        default: e = launch_tc2<64>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
+        case 256: e = launch_tc2<256>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, p.splits, epi); break;
+        case 128: e = launch_tc2<128>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, p.splits, epi); break;
+        default: e = launch_tc2<64>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, p.splits, epi); break;
       }
     } else {
       switch (p.bn) {
-        case 256: e = launch_tc<256>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
-        case 128: e = launch_tc<128>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
-        default: e = launch_tc<64>(c, ma, mb, M, N, K, az, bz, p.splits, epi); break;
+        case 256: e = launch_tc<256>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, p.splits, epi); break;
+        case 128: e = launch_tc<128>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, p.splits, epi); break;
+        default: e = launch_tc<64>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, p.splits, epi); break;
       }
     }
     CUDA_OR_FAIL(c, e);
@@ -440,7 +458,12 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
   const S* b = static_cast<const S*>(B.ptr) + (long)bz * B.zstride;
   const int kps = (int)rup((K + p.splits - 1) / p.splits, 32);
   dim3 grid((N + 63) / 64, (M + 127) / 128, p.splits);
-  gemm_simt_kernel<S, Epi><<<grid, 128, 0, c->stream>>>(a, A.ld, b, B.ld, M, N, K, kps, epi);
+  int dsm = 0;
+  if constexpr (IsTile<Epi>::value) {
+    dsm = tile_smem_bytes(64);
+    CUDA_OR_FAIL(c, cudaFuncSetAttribute(gemm_simt_kernel<S, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm));
+  }
+  gemm_simt_kernel<S, Epi><<<grid, 128, dsm, c->stream>>>(a, A.ld, b, B.ld, M, N, K, kps, epi);
   count_launch(c);
   CUDA_OR_FAIL(c, cudaGetLastError());
   return MLSTM_OK;
@@ -510,10 +533,12 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
     RET_IF(gemm<S>(c, A, 0, Bo, 0, 256, 5 * h, e, plan_gemm(c->tc, 256, 5 * h, e, false), EpiTab<S>{n}));
   }
   phase(c, PH_FWD);
-  const Opd Hprev{n.Hrm, B, h, h, T + 1, (long)B * h};
-  const Opd Wmh{n.Wmh_w, h, h, h, 1, (long)h * h};
-  const Opd Msc{n.Mscr, B, h, h, 1, (long)B * h};
-  const Opd Wh{n.Wh_w, 4L * h, h, h, 1, 4L * h * h};
+  // L2 policy: the recurrent weights are re-read every timestep -- keep W_mh and a fraction of
+  // W_h resident (evict_last); the activations are read once (evict_first).
+  const Opd Hprev{n.Hrm, B, h, h, T + 1, (long)B * h, kPolFirst};
+  const Opd Wmh{n.Wmh_w, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh)};
+  const Opd Msc{n.Mscr, B, h, h, 1, (long)B * h, kPolFirst};
+  const Opd Wh{n.Wh_w, 4L * h, h, h, 1, 4L * h * h, pol_last(c->l2_wh)};
   const Plan p1 = plan_gemm(c->tc, B, h, h, false), p2 = plan_gemm(c->tc, B, 4 * h, h, false);
   for (int t = 0; t < T; ++t) {
     RET_IF(gemm<S>(c, Hprev, t, Wmh, 0, B, h, h, p1, EpiF1<S>{n, t}));
@@ -551,10 +576,10 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
   phase(c, PH_BWD);
   LAUNCH(c, (gate_bwd_last_kernel<S><<<grid_for((long)B * h / 16), 256, 0, c->stream>>>(n)));
   {
-    const Opd dZ{n.dZscr, B, 4L * h, 4L * h, 1, 4L * B * h};
-    const Opd WhT{n.WhT, h, 4L * h, 4L * h, 1, 4L * h * h};
-    const Opd dA{n.dAscr, B, h, h, 1, (long)B * h};
-    const Opd WmhT{n.WmhT, h, h, h, 1, (long)h * h};
+    const Opd dZ{n.dZscr, B, 4L * h, 4L * h, 1, 4L * B * h, kPolFirst};
+    const Opd WhT{n.WhT, h, 4L * h, 4L * h, 1, 4L * h * h, pol_last(c->l2_wh)};
+    const Opd dA{n.dAscr, B, h, h, 1, (long)B * h, kPolFirst};
+    const Opd WmhT{n.WmhT, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh)};
     const Plan p1 = plan_gemm(c->tc, B, h, 4 * h, false), p2 = plan_gemm(c->tc, B, h, h, false);
     for (int t = T - 1; t >= 0; --t) {
       RET_IF(gemm<S>(c, dZ, 0, WhT, 0, B, h, 4 * h, p1, EpiB1<S>{n, t}));
@@ -1198,6 +1223,42 @@ mlstm_status mlstm_gemm_bench(int engine, int M, int N, int K, int bn, int iters
   cudaEventDestroy(e1);
   cleanup();
   return st;
+}
+
+namespace {
+TraceRec* g_trace_host_buf = nullptr;
+}
+
+mlstm_status mlstm_trace_enable(int capacity) {
+  if (g_trace_host_buf) {
+    cudaFree(g_trace_host_buf);
+    g_trace_host_buf = nullptr;
+  }
+  TraceRec* p = nullptr;
+  unsigned int cap = capacity > 0 ? (unsigned int)capacity : 0u, zero = 0;
+  if (cap && cudaMalloc(&p, sizeof(TraceRec) * cap) != cudaSuccess) return fail(MLSTM_ECUDA, "cudaMalloc trace");
+  g_trace_host_buf = p;
+  if (cudaMemcpyToSymbol(g_trace, &p, sizeof p) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_trace_cap, &cap, sizeof cap) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_trace_n, &zero, sizeof zero) != cudaSuccess)
+    return fail(MLSTM_ECUDA, "trace symbols");
+  return MLSTM_OK;
+}
+
+mlstm_status mlstm_trace_read(uint64_t* out, int capacity, int* n) {
+  if (!out || !n) return fail(MLSTM_EINVAL, "null argument");
+  unsigned int cnt = 0, zero = 0;
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpyFromSymbol(&cnt, g_trace_n, sizeof cnt) != cudaSuccess)
+    return fail(MLSTM_ECUDA, "trace count");
+  unsigned int cap = 0;
+  cudaMemcpyFromSymbol(&cap, g_trace_cap, sizeof cap);
+  cnt = std::min(cnt, cap);
+  cnt = std::min(cnt, (unsigned int)std::max(capacity, 0));
+  if (cnt && cudaMemcpy(out, g_trace_host_buf, sizeof(TraceRec) * cnt, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(MLSTM_ECUDA, "trace copy");
+  cudaMemcpyToSymbol(g_trace_n, &zero, sizeof zero);
+  *n = (int)cnt;
+  return MLSTM_OK;
 }
 
 const char* mlstm_last_error(void) { return g_err.c_str(); }

@@ -144,4 +144,29 @@ __device__ __forceinline__ void ld16(const float* src, float* v) {
 
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-x)); }
 
+// Gate nonlinearities.  Mixed mode (S = __half): the hardware tanh.approx.f32 (MUFU, max relative
+// error ~2^-11, below the fp16 resolution the gates are stored at) and sigma(x) = tanh(x/2)/2 + 1/2.
+// fp32 parity mode (S = float): IEEE expf/tanhf.
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+template <typename S>
+__device__ __forceinline__ float act_tanh(float x) {
+  return tanhf(x);
+}
+template <>
+__device__ __forceinline__ float act_tanh<__half>(float x) {
+  return tanh_approx(x);
+}
+template <typename S>
+__device__ __forceinline__ float act_sigmoid(float x) {
+  return sigmoidf_(x);
+}
+template <>
+__device__ __forceinline__ float act_sigmoid<__half>(float x) {
+  return fmaf(0.5f, tanh_approx(0.5f * x), 0.5f);
+}
+
 }  // namespace mlstm

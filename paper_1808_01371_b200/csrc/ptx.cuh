@@ -61,6 +61,22 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// Operand policy code (host-chosen per GEMM operand): bits 8-9 = priority of the first `fraction`
+// of lines (0 normal, 1 evict_first, 2 evict_last), bits 0-7 = fraction * 255; lines outside the
+// fraction are evict_first.
+__device__ __forceinline__ uint64_t make_policy(uint32_t code) {
+  const uint32_t prio = (code >> 8) & 3;
+  const float frac = (float)(code & 255) / 255.f;
+  uint64_t p;
+  if (prio == 2) {
+    asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(p) : "f"(frac));
+  } else if (prio == 1) {
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  } else {
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  }
+  return p;
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -202,6 +218,12 @@ __device__ __forceinline__ void mma_commit_2sm_mc(uint64_t* bar, uint16_t mask) 
           smem_u32(bar)),
       "h"(mask)
       : "memory");
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 }  // namespace ptx

@@ -15,7 +15,7 @@ import re
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmlstm.so")
+LIB_PATH = os.environ.get("MLSTM_LIB") or os.path.join(HERE, "libmlstm.so")  # MLSTM_LIB: A/B experiments
 HEADER = os.path.join(os.path.dirname(HERE), "include", "mlstm.h")
 
 MLSTM_OK, MLSTM_EINVAL, MLSTM_ECUDA, MLSTM_ENCCL, MLSTM_ENOMEM, MLSTM_ESTATE, MLSTM_EDIVERGED = range(7)
@@ -90,6 +90,8 @@ _SIGS = {
     "mlstm_launches_per_step": (ctypes.c_int32, [_vp]),
     "mlstm_gemm_bench": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, _dp]),
+    "mlstm_trace_enable": (ctypes.c_int, [ctypes.c_int]),
+    "mlstm_trace_read": (ctypes.c_int, [_P(ctypes.c_uint64), ctypes.c_int, _i32p]),
     "mlstm_last_error": (ctypes.c_char_p, []),
     "mlstm_destroy": (None, [_vp]),
 }
@@ -206,6 +208,17 @@ def mlstm_gemm_bench(engine: int, M: int, N: int, K: int, bn: int = 0, iters: in
     ms = ctypes.c_double()
     _check(lib().mlstm_gemm_bench(engine, M, N, K, bn, iters, ctypes.byref(ms)))
     return ms.value
+
+
+def mlstm_trace_enable(capacity: int) -> None:
+    _check(lib().mlstm_trace_enable(capacity))
+
+
+def mlstm_trace_read(capacity: int = 1 << 20) -> np.ndarray:
+    out = np.zeros((capacity, 8), dtype=np.uint64)
+    n = ctypes.c_int32()
+    _check(lib().mlstm_trace_read(out.ctypes.data_as(_P(ctypes.c_uint64)), capacity, ctypes.byref(n)))
+    return out[: n.value]
 
 
 def mlstm_destroy(ctx):

@@ -1,0 +1,11 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
+{
+timeout 120 python tools/diag_step.py mixed 1024 64 256 16 || echo "DIAG FAILED rc=$?"
+timeout 120 python tools/diag_step.py mixed 128 64 130 5 || echo "DIAG FAILED rc=$?"
+timeout 120 python tools/diag_step.py fp32 128 64 130 5 || echo "DIAG FAILED rc=$?"
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -15
+timeout 600 python tools/trace_step.py 2>&1 | grep -v Warn | grep -v nanmean
+timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline
+} > gpurun_out/run5.log 2>&1
+tail -40 gpurun_out/run5.log
