@@ -1,20 +1,28 @@
-// gemm.cuh -- the two GEMM engines every contraction of the step runs on.
+// gemm.cuh -- the GEMM engines every contraction of the step runs on.
 //
 //   D[M x N] = A[M x K] . B[N x K]^T   (both operands K-major, i.e. row-major with K contiguous),
-//   fp32 accumulation, result handed to a fused epilogue functor 64 columns at a time:
-//       epi(row, col0, float (&v)[64])   with v[i] = D[row][col0 + i].
+//   fp32 accumulation, result handed to a fused epilogue functor 16*NG columns at a time:
+//       epi.run<NG>(row, col0, v)   with v[i] = D[row][col0 + i], i < 16*NG.
 //
-// * gemm_tc_kernel (mixed precision, fp16 operands): TMA (128B swizzle) -> multi-stage mbarrier
-//   ring in shared memory -> single-thread tcgen05.mma (M=128, N=BN, K=16) into a TMEM fp32
-//   accumulator -> 4 epilogue warps tcgen05.ld their 32 TMEM lanes (one accumulator row per
-//   thread).  Warp roles: warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer, warps 2-5
-//   epilogue.  One output tile per CTA; optional split-K over blockIdx.z.
-// * gemm_simt_kernel (fp32 parity mode, "single precision"): plain FFMA, 128 x 64 tile,
-//   one output row per thread, fixed ascending-k accumulation -- same epilogue interface.
+// tcgen05 engines (mixed precision, fp16 operands).  Warp roles: warp 0 TMA producer, warp 1 TMEM
+// allocator + single-thread MMA issuer, warps 2..9 epilogue (two warps per TMEM lane quarter, so
+// the memory-heavy fused epilogues -- on the recurrence's critical path -- get 8 warps).
+//   * gemm_tc_kernel   one CTA per 128 x BN tile (M=128 tcgen05.mma).
+//   * gemm_tc2_kernel  a CTA pair (cluster of 2, cta_group::2) per 256 x BN tile: each CTA stages
+//                      its 128 rows of A and BN/2 rows of B, halving per-SM operand traffic.
+//   * gemm_tc1s_kernel one CTA per 128 x 256 tile with the K loop split S ways over a cluster of S
+//                      CTAs, reduced in-kernel through an L2 scratch in fixed order.
+//   Pipeline: TMA (128B swizzle) -> STAGES-deep mbarrier ring -> MMA into a TMEM fp32 accumulator
+//   -> tcgen05.ld by the epilogue warps.  Measured engine choice: profiles/r01_gemm_sweep.log.
+// SIMT engine (fp32 parity mode, "single precision"): plain FFMA, 128 x 64 tile.
 #pragma once
 #include "ptx.cuh"
 
 namespace mlstm {
+
+constexpr int kEpiWarps = 8;
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
+constexpr int kGemmStaticB = 1;  // B operand is a weight untouched by the preceding kernels
 
 // ---- optional intra-kernel timeline (mlstm_trace_enable): one record per CTA,
 // {tag, cta, t_start, t_first_tma, t_first_full, t_acc_ready, t_reduced, t_end} in ns.
@@ -24,10 +32,6 @@ struct TraceRec {
 __device__ TraceRec* g_trace = nullptr;
 __device__ unsigned int g_trace_n = 0;
 __device__ unsigned int g_trace_cap = 0;
-struct Trace {
-  uint64_t t[6];
-  __device__ __forceinline__ void mark(int i) { t[i] = ptx::globaltimer(); }
-};
 __device__ __forceinline__ void trace_flush(const uint64_t* ts, int tag) {
   TraceRec* tr = g_trace;
   if (!tr) return;
@@ -39,48 +43,13 @@ __device__ __forceinline__ void trace_flush(const uint64_t* ts, int tag) {
   for (int k = 0; k < 6; ++k) r.v[2 + k] = ts[k];
   tr[i] = r;
 }
-__device__ __forceinline__ void epi_bar_() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-template <class E, class = void>
-struct IsTile {  // epilogue with a cooperative tile() member (see epilogues.cuh)
-  static constexpr bool value = false;
-};
-template <class E>
-struct IsTile<E, decltype(void(E::kTile))> {
-  static constexpr bool value = E::kTile;
-};
-
-// Stages a 128 x (64*nchunk) fp32 accumulator tile from TMEM into shared memory (row stride ldt):
-// thread = TMEM lane = tile row.
-__device__ __forceinline__ void stage_tmem_rows(float* T, int ldt, uint32_t tmem, int q, int lane, int nchunk,
-                                                bool have) {
-  const int rl = q * 32 + lane;
-#pragma unroll 1
-  for (int c = 0; c < nchunk; ++c) {
-    float v[64];
-    if (have) {
-      const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 64;
-      ptx::tmem_ld16(ta, v);
-      ptx::tmem_ld16(ta + 16, v + 16);
-      ptx::tmem_ld16(ta + 32, v + 32);
-      ptx::tmem_ld16(ta + 48, v + 48);
-      ptx::tmem_ld_wait();
-    } else {
-#pragma unroll
-      for (int i = 0; i < 64; ++i) v[i] = 0.f;
-    }
-    float4* dst = reinterpret_cast<float4*>(T + rl * ldt + c * 64);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-  }
-}
-
 template <class Epi>
 struct EpiTag {
   static constexpr int value = 0;
 };
 
 template <int BN>
-struct TcCfg {
+struct TcCfg {  // one CTA per 128 x BN tile
   static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
@@ -88,150 +57,9 @@ struct TcCfg {
   static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
-
-template <int BN, class Epi>
-__global__ void __launch_bounds__(192, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                   int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, Epi epi) {
-  using C = TcCfg<BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* accf = empty + C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
-  __shared__ uint64_t tr_ts[6];
-  const bool tracing = g_trace != nullptr;
-  if (tracing && threadIdx.x == 0) {
-    for (int k = 1; k < 6; ++k) tr_ts[k] = 0;
-    tr_ts[0] = ptx::globaltimer();
-  }
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * C::BM, n0 = blockIdx.x * BN;
-  const int total_kb = (K + C::BK - 1) / C::BK;
-  const int kb0 = blockIdx.z * kb_per_split;
-  const int nkb = max(0, min(kb_per_split, total_kb - kb0));
-
-  if (threadIdx.x == 0) {
-#pragma unroll 1
-    for (int s = 0; s < C::STAGES; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
-    }
-    ptx::mbar_init(accf, 1);
-    ptx::fence_barrier_init();
-  }
-  if (warp == 1) {
-    ptx::tmem_alloc(tmem_slot, BN);
-    ptx::tmem_relinquish();
-  }
-  if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tmA);
-    ptx::prefetch_tmap(&tmB);
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0 && nkb > 0) {
-      const uint64_t pa = ptx::make_policy(polA), pb = ptx::make_policy(polB);
-#pragma unroll 1
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % C::STAGES;
-        const uint32_t ph = (i / C::STAGES) & 1;
-        ptx::mbar_wait(&empty[s], ph ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
-        const int kc = (kb0 + i) * C::BK;
-        if (tracing && i == 0) tr_ts[1] = ptx::globaltimer();
-        ptx::tma_load_3d(sA + s * C::A_BYTES, &tmA, &full[s], kc, m0, az, pa);
-        ptx::tma_load_3d(sB + s * C::B_BYTES, &tmB, &full[s], kc, n0, bz, pb);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && nkb > 0) {
-      constexpr uint32_t idesc = ptx::idesc_f16_f32(C::BM, BN);
-#pragma unroll 1
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % C::STAGES;
-        const uint32_t ph = (i / C::STAGES) & 1;
-        ptx::mbar_wait(&full[s], ph);
-        ptx::tc_fence_after();
-        if (tracing && i == 0) tr_ts[2] = ptx::globaltimer();
-        const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
-        const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
-#pragma unroll
-        for (int k = 0; k < C::BK / 16; ++k)
-          ptx::mma_f16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
-        ptx::mma_commit(&empty[s]);
-      }
-      ptx::mma_commit(accf);
-    }
-  } else {
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = m0 + q * 32 + lane;
-    if (nkb > 0) {
-      ptx::mbar_wait(accf, 0);
-      ptx::tc_fence_after();
-    }
-    if (tracing && threadIdx.x == 64) tr_ts[3] = ptx::globaltimer();
-    if constexpr (IsTile<Epi>::value) {
-      float* T = reinterpret_cast<float*>(smem);  // the pipeline stages are idle now
-      constexpr int ldt = BN + 4;
-      stage_tmem_rows(T, ldt, tmem, q, lane, BN / 64, nkb > 0);
-      ptx::tc_fence_before();
-      epi_bar_();
-      const int rows = min(128, M - (row - q * 32 - lane));
-      if (rows > 0 && n0 < N)
-        epi.tile(T, ldt, row - q * 32 - lane, n0, min(BN, N - n0), rows,
-                 reinterpret_cast<uint8_t*>(T + 128 * ldt), (int)threadIdx.x - 64);
-    } else {
-#pragma unroll 1
-    for (int c = 0; c < BN / 64; ++c) {
-      float v[64];
-      if (nkb > 0) {
-        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 64;
-        ptx::tmem_ld16(ta, v);
-        ptx::tmem_ld16(ta + 16, v + 16);
-        ptx::tmem_ld16(ta + 32, v + 32);
-        ptx::tmem_ld16(ta + 48, v + 48);
-        ptx::tmem_ld_wait();
-      } else {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) v[i] = 0.f;
-      }
-      const int col0 = n0 + c * 64;
-      if (row < M && col0 < N) epi(row, col0, v);
-    }
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (tracing && threadIdx.x == 0) {
-    tr_ts[5] = ptx::globaltimer();
-    trace_flush(tr_ts, EpiTag<Epi>::value);
-  }
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, BN);
-  }
-}
-
-
-// ---------------------------------------------------------------------------------------------
-// gemm_tc2_kernel: the same contract with a CTA pair (cluster of 2, tcgen05 cta_group::2) per
-// 256 x BN output tile.  Each CTA stages its 128 rows of A and BN/2 rows of B per k-block, so a
-// CTA pulls (128 + BN/2) x 64 x 2 bytes per 256 x BN x 64 of MMA work: half the operand traffic per
-// FLOP of the 1-CTA tile -- the L2 -> SM path is what bounds these GEMMs.  Both CTAs' TMA loads
-// count on the leader's full barrier; the leader's single thread issues the M=256 MMA; its commit
-// multicasts to both CTAs' empty / accumulator barriers; each CTA's epilogue reads its own TMEM.
 template <int BN>
-struct Tc2Cfg {
-  static constexpr int BM = 128, BK = 64;  // rows per CTA
+struct Tc2Cfg {  // CTA pair per 256 x BN tile: per CTA 128 rows of A, BN/2 rows of B
+  static constexpr int BM = 128, BK = 64;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -239,26 +67,219 @@ struct Tc2Cfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
-template <int BN, class Epi>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
-    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                    int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, Epi epi) {
-  using C = Tc2Cfg<BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* accf = empty + C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
-  __shared__ uint64_t tr_ts[6];
-  const bool tracing = g_trace != nullptr;
-  if (tracing && threadIdx.x == 0) {
-    for (int k = 1; k < 6; ++k) tr_ts[k] = 0;
-    tr_ts[0] = ptx::globaltimer();
+// Shared-memory carve-up common to the tcgen05 kernels.
+template <class C>
+struct SmemLayout {
+  uint8_t *sA, *sB;
+  uint64_t *full, *empty, *accf;
+  uint32_t* tmem_slot;
+  __device__ __forceinline__ explicit SmemLayout(uint8_t* smem_raw) {
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    sA = smem;
+    sB = smem + C::STAGES * C::A_BYTES;
+    full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+    empty = full + C::STAGES;
+    accf = empty + C::STAGES;
+    tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  }
+};
+
+// Barrier init (thread 0), TMEM allocation (warp 1) and descriptor prefetch (warp 0).
+template <class C, bool PAIR>
+__device__ __forceinline__ void gemm_setup(const SmemLayout<C>& L, const CUtensorMap* tmA, const CUtensorMap* tmB,
+                                           int ncols) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+#pragma unroll 1
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&L.full[s], 1);   // one arrive.expect_tx per phase (the pair leader's in PAIR mode)
+      ptx::mbar_init(&L.empty[s], 1);  // the MMA commit (multicast to both CTAs in PAIR mode)
+    }
+    ptx::mbar_init(L.accf, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    if (PAIR) {
+      ptx::tmem_alloc2(L.tmem_slot, ncols);
+      ptx::tmem_relinquish2();
+    } else {
+      ptx::tmem_alloc(L.tmem_slot, ncols);
+      ptx::tmem_relinquish();
+    }
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(tmA);
+    ptx::prefetch_tmap(tmB);
+  }
+}
+
+// TMA producer (one thread).  With kGemmStaticB the B operand (a weight) does not depend on the
+// preceding kernel: its first stages are fetched before the grid-dependency wait (overlapping the
+// previous kernel's tail under programmatic dependent launch); the A operand after it.
+// PAIR: both CTAs load their halves and count bytes on the leader's barrier (bar_leader0 = its
+// full[0] in shared::cluster space); only the leader arrives, with both CTAs' byte count -- the
+// peer's bytes may land first (transiently negative tx-count); the peer cannot run a phase ahead
+// because it waits on its own empty barrier, released by the same multicast commit.  (A
+// release.cluster remote arrive here would fence every prior TMA and serialise the pipeline.)
+template <class C, bool PAIR>
+__device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUtensorMap* tmA, const CUtensorMap* tmB,
+                                             int nkb, int kb0, int m0, int nb0, int az, int bz, uint32_t polA,
+                                             uint32_t polB, int flags, bool leader, uint32_t bar_leader0,
+                                             uint64_t* trace_slot) {
+  const uint64_t pa = ptx::make_policy(polA), pb = ptx::make_policy(polB);
+  const uint32_t tx = PAIR ? 2 * C::STAGE_BYTES : C::STAGE_BYTES;
+  auto loadA = [&](int s, int kb) {
+    if (PAIR) ptx::tma_load_3d_2sm(L.sA + s * C::A_BYTES, tmA, bar_leader0 + s * 8, kb * C::BK, m0, az, pa);
+    else ptx::tma_load_3d(L.sA + s * C::A_BYTES, tmA, &L.full[s], kb * C::BK, m0, az, pa);
+  };
+  auto loadB = [&](int s, int kb) {
+    if (PAIR) ptx::tma_load_3d_2sm(L.sB + s * C::B_BYTES, tmB, bar_leader0 + s * 8, kb * C::BK, nb0, bz, pb);
+    else ptx::tma_load_3d(L.sB + s * C::B_BYTES, tmB, &L.full[s], kb * C::BK, nb0, bz, pb);
+  };
+  const int pre = (flags & kGemmStaticB) ? min(C::STAGES, nkb) : 0;
+  for (int i = 0; i < pre; ++i) {
+    if (leader) ptx::mbar_arrive_expect_tx(&L.full[i], tx);
+    loadB(i, kb0 + i);
+  }
+  ptx::pdl_wait();
+  if (trace_slot) *trace_slot = ptx::globaltimer();
+  for (int i = 0; i < pre; ++i) loadA(i, kb0 + i);
+#pragma unroll 1
+  for (int i = pre; i < nkb; ++i) {
+    const int s = i % C::STAGES;
+    const uint32_t ph = (i / C::STAGES) & 1;
+    ptx::mbar_wait(&L.empty[s], ph ^ 1);
+    if (leader) ptx::mbar_arrive_expect_tx(&L.full[s], tx);
+    loadA(s, kb0 + i);
+    loadB(s, kb0 + i);
+  }
+}
+
+// MMA issuer (one thread of the leader CTA): BK/16 tcgen05.mma per stage, commit frees the stage;
+// the final commit signals the accumulator.  PAIR: M = 256 over the CTA pair, commits multicast.
+template <class C, bool PAIR, int MMA_N>
+__device__ __forceinline__ void gemm_mma(const SmemLayout<C>& L, uint32_t tmem, int nkb, uint16_t pair_mask,
+                                         uint64_t* trace_slot) {
+  constexpr uint32_t idesc = ptx::idesc_f16_f32(PAIR ? 256 : 128, MMA_N);
+#pragma unroll 1
+  for (int i = 0; i < nkb; ++i) {
+    const int s = i % C::STAGES;
+    const uint32_t ph = (i / C::STAGES) & 1;
+    ptx::mbar_wait(&L.full[s], ph);
+    ptx::tc_fence_after();
+    if (trace_slot && i == 0) *trace_slot = ptx::globaltimer();
+    const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(L.sA + s * C::A_BYTES));
+    const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(L.sB + s * C::B_BYTES));
+#pragma unroll
+    for (int k = 0; k < C::BK / 16; ++k) {
+      if (PAIR) ptx::mma_f16_2sm(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
+      else ptx::mma_f16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
+    }
+    if (PAIR) ptx::mma_commit_2sm_mc(&L.empty[s], pair_mask);
+    else ptx::mma_commit(&L.empty[s]);
+  }
+  if (PAIR) ptx::mma_commit_2sm_mc(L.accf, pair_mask);
+  else ptx::mma_commit(L.accf);
+}
+
+// 64 accumulator columns of this thread's TMEM lane (zeros if the CTA had no k-blocks).
+__device__ __forceinline__ void tmem_chunk(uint32_t tmem, int q, int c, bool have, float* v) {
+  if (have) {
+    const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 64;
+    ptx::tmem_ld16(ta, v);
+    ptx::tmem_ld16(ta + 16, v + 16);
+    ptx::tmem_ld16(ta + 32, v + 32);
+    ptx::tmem_ld16(ta + 48, v + 48);
+    ptx::tmem_ld_wait();
+  } else {
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] = 0.f;
+  }
+}
+
+// Epilogue warps' common start: wait for the accumulator, then for the preceding grid (inputs
+// of the fused epilogue), and let the next kernel's prologue start.
+__device__ __forceinline__ void epi_begin(uint64_t* accf, bool have, uint64_t* trace_slot) {
+  if (have) {
+    ptx::mbar_wait(accf, 0);
+    ptx::tc_fence_after();
+  }
+  if (trace_slot && threadIdx.x == 64) *trace_slot = ptx::globaltimer();
+  ptx::pdl_wait();
+  if (threadIdx.x == 64) ptx::pdl_trigger();
+}
+
+#define MLSTM_TRACE_BEGIN()                                  \
+  __shared__ uint64_t tr_ts[6];                              \
+  const bool tracing = g_trace != nullptr;                   \
+  if (tracing && threadIdx.x == 0) {                         \
+    for (int k = 1; k < 6; ++k) tr_ts[k] = 0;                \
+    tr_ts[0] = ptx::globaltimer();                           \
+  }
+#define MLSTM_TRACE_SLOT(i) (tracing ? &tr_ts[i] : nullptr)
+#define MLSTM_TRACE_END()                                    \
+  if (tracing && threadIdx.x == 0) {                         \
+    tr_ts[5] = ptx::globaltimer();                           \
+    trace_flush(tr_ts, EpiTag<Epi>::value);                  \
   }
 
+// ---------------------------------------------------------------------------------------------
+template <int BN, class Epi>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                   int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, int flags,
+                   Epi epi) {
+  using C = TcCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  const SmemLayout<C> L(smem_raw);
+  MLSTM_TRACE_BEGIN();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * C::BM, n0 = blockIdx.x * BN;
+  const int total_kb = (K + C::BK - 1) / C::BK;
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int nkb = max(0, min(kb_per_split, total_kb - kb0));
+  gemm_setup<C, false>(L, &tmA, &tmB, BN);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *L.tmem_slot;
+  if (warp == 0) {
+    if (lane == 0 && nkb > 0)
+      gemm_produce<C, false>(L, &tmA, &tmB, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true, 0,
+                             MLSTM_TRACE_SLOT(1));
+  } else if (warp == 1) {
+    if (lane == 0 && nkb > 0) gemm_mma<C, false, BN>(L, tmem, nkb, 0, MLSTM_TRACE_SLOT(2));
+  } else {
+    const int q = warp & 3, grp = (warp - 2) >> 2;
+    const int row = m0 + q * 32 + lane;
+    epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
+#pragma unroll 1
+    for (int c = grp; c < BN / 64; c += 2) {
+      float v[64];
+      tmem_chunk(tmem, q, c, nkb > 0, v);
+      const int col0 = n0 + c * 64;
+      if (row < M && col0 < N) epi.template run<4>(row, col0, v);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  MLSTM_TRACE_END();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, BN);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+template <int BN, class Epi>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                    int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, int flags,
+                    Epi epi) {
+  using C = Tc2Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  const SmemLayout<C> L(smem_raw);
+  MLSTM_TRACE_BEGIN();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
   const bool leader = rank == 0;
@@ -267,112 +288,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   const int total_kb = (K + C::BK - 1) / C::BK;
   const int kb0 = blockIdx.z * kb_per_split;
   const int nkb = max(0, min(kb_per_split, total_kb - kb0));
-
-  if (threadIdx.x == 0) {
-#pragma unroll 1
-    for (int s = 0; s < C::STAGES; ++s) {
-      ptx::mbar_init(&full[s], 1);   // leader's arrive.expect_tx covers both CTAs' bytes
-      ptx::mbar_init(&empty[s], 1);  // leader's multicast commit
-    }
-    ptx::mbar_init(accf, 1);
-    ptx::fence_barrier_init();
-  }
-  if (warp == 1) {
-    ptx::tmem_alloc2(tmem_slot, BN);
-    ptx::tmem_relinquish2();
-  }
-  if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tmA);
-    ptx::prefetch_tmap(&tmB);
-  }
+  gemm_setup<C, true>(L, &tmA, &tmB, BN);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
+  const uint32_t tmem = *L.tmem_slot;
   if (warp == 0) {
-    if (lane == 0 && nkb > 0) {
-      const uint64_t pa = ptx::make_policy(polA), pb = ptx::make_policy(polB);
-      const uint32_t full_leader0 = ptx::mapa_shared(ptx::smem_u32(&full[0]), 0);
-#pragma unroll 1
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % C::STAGES;
-        const uint32_t ph = (i / C::STAGES) & 1;
-        ptx::mbar_wait(&empty[s], ph ^ 1);
-        // Only the leader arrives (with both CTAs' byte count).  The peer's bytes may land first and
-        // drive the tx-count transiently negative; the phase cannot complete before the leader's
-        // arrive, and the peer cannot run a phase ahead (it waits on its own empty barrier, released
-        // by the same commit).  A release.cluster remote arrive here would fence every prior TMA.
-        if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * C::STAGE_BYTES);
-        const int kc = (kb0 + i) * C::BK;
-        if (tracing && i == 0) tr_ts[1] = ptx::globaltimer();
-        ptx::tma_load_3d_2sm(sA + s * C::A_BYTES, &tmA, full_leader0 + s * 8, kc, m0, az, pa);
-        ptx::tma_load_3d_2sm(sB + s * C::B_BYTES, &tmB, full_leader0 + s * 8, kc, n0 + rank * (BN / 2), bz, pb);
-      }
-    }
+    if (lane == 0 && nkb > 0)
+      gemm_produce<C, true>(L, &tmA, &tmB, nkb, kb0, m0, n0 + rank * (BN / 2), az, bz, polA, polB, flags, leader,
+                            ptx::mapa_shared(ptx::smem_u32(&L.full[0]), 0), MLSTM_TRACE_SLOT(1));
   } else if (warp == 1) {
-    if (leader && lane == 0 && nkb > 0) {
-      constexpr uint32_t idesc = ptx::idesc_f16_f32(256, BN);
-#pragma unroll 1
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % C::STAGES;
-        const uint32_t ph = (i / C::STAGES) & 1;
-        ptx::mbar_wait(&full[s], ph);
-        ptx::tc_fence_after();
-        if (tracing && i == 0) tr_ts[2] = ptx::globaltimer();
-        const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
-        const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
-#pragma unroll
-        for (int k = 0; k < C::BK / 16; ++k)
-          ptx::mma_f16_2sm(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
-        ptx::mma_commit_2sm_mc(&empty[s], 0x3);
-      }
-      ptx::mma_commit_2sm_mc(accf, 0x3);
-    }
+    if (leader && lane == 0 && nkb > 0) gemm_mma<C, true, BN>(L, tmem, nkb, 0x3, MLSTM_TRACE_SLOT(2));
   } else {
-    const int q = warp & 3;
+    const int q = warp & 3, grp = (warp - 2) >> 2;
     const int row = m0 + q * 32 + lane;
-    if (nkb > 0) {
-      ptx::mbar_wait(accf, 0);
-      ptx::tc_fence_after();
-    }
-    if (tracing && threadIdx.x == 64) tr_ts[3] = ptx::globaltimer();
-    if constexpr (IsTile<Epi>::value) {
-      float* T = reinterpret_cast<float*>(smem);  // the pipeline stages are idle now
-      constexpr int ldt = BN + 4;
-      stage_tmem_rows(T, ldt, tmem, q, lane, BN / 64, nkb > 0);
-      ptx::tc_fence_before();
-      epi_bar_();
-      const int rows = min(128, M - (row - q * 32 - lane));
-      if (rows > 0 && n0 < N)
-        epi.tile(T, ldt, row - q * 32 - lane, n0, min(BN, N - n0), rows,
-                 reinterpret_cast<uint8_t*>(T + 128 * ldt), (int)threadIdx.x - 64);
-    } else {
+    epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
 #pragma unroll 1
-    for (int c = 0; c < BN / 64; ++c) {
+    for (int c = grp; c < BN / 64; c += 2) {
       float v[64];
-      if (nkb > 0) {
-        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 64;
-        ptx::tmem_ld16(ta, v);
-        ptx::tmem_ld16(ta + 16, v + 16);
-        ptx::tmem_ld16(ta + 32, v + 32);
-        ptx::tmem_ld16(ta + 48, v + 48);
-        ptx::tmem_ld_wait();
-      } else {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) v[i] = 0.f;
-      }
+      tmem_chunk(tmem, q, c, nkb > 0, v);
       const int col0 = n0 + c * 64;
-      if (row < M && col0 < N) epi(row, col0, v);
-    }
+      if (row < M && col0 < N) epi.template run<4>(row, col0, v);
     }
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();
-  if (tracing && threadIdx.x == 0) {
-    tr_ts[5] = ptx::globaltimer();
-    trace_flush(tr_ts, EpiTag<Epi>::value);
-  }
+  MLSTM_TRACE_END();
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc2(tmem, BN);
@@ -380,207 +321,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 }
 
 // ---------------------------------------------------------------------------------------------
-// gemm_tc2s_kernel: CTA-pair 256 x 256 tiles with the K loop split S ways across S pairs of one
-// cluster (2S CTAs; cluster rank r: row half r & 1, K-split r >> 1).  Used where the output is too
-// small to fill the machine with 256-wide tiles (the per-timestep GEMMs with N = h).  After the
-// mainloop every CTA stages its fp32 partial in its own (now idle) pipeline shared memory; after a
-// cluster barrier, CTA r reduces columns [z*256/S, (z+1)*256/S) of its 128 rows over the S
-// partials through DSMEM in fixed order z = 0..S-1 (deterministic) and runs the fused epilogue on
-// that slice -- so the epilogue work stays spread over all 2S CTAs.
+// Split-K over a cluster of S CTAs (rank z = K split).  Each CTA writes its fp32 partial to an
+// L2-resident scratch laid out [z][float4 column group (64)][row (128)] (lanes = rows: coalesced);
+// after the cluster barrier (release/acquire at cluster scope orders those writes) CTA z sums
+// columns [z*256/S, (z+1)*256/S) of its 128 rows over the S partials in fixed order z' = 0..S-1
+// (deterministic) and runs the fused epilogue on that slice -- the 256 epilogue threads each take
+// half a row of the slice, or a whole row when the epilogue needs full 64-column chunks.
 template <int S, class Epi>
-__global__ void __launch_bounds__(192, 1)
-    gemm_tc2s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                     int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, Epi epi) {
-  constexpr int BN = 256;
-  using C = Tc2Cfg<BN>;
-  constexpr int SLICE = BN / S;
-  constexpr int LDS = BN + 4;  // staging row stride in floats (odd number of 16-byte units)
-  static_assert(128 * LDS * 4 <= C::STAGES * C::STAGE_BYTES, "staging must fit in the pipeline smem");
-  static_assert(SLICE % 64 == 0, "slice is a whole number of epilogue chunks");
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  float* stage = reinterpret_cast<float*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* accf = empty + C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
-  __shared__ uint64_t tr_ts[6];
-  const bool tracing = g_trace != nullptr;
-  if (tracing && threadIdx.x == 0) {
-    for (int k = 1; k < 6; ++k) tr_ts[k] = 0;
-    tr_ts[0] = ptx::globaltimer();
-  }
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = ptx::cluster_ctarank();
-  const uint32_t half = rank & 1u, z = rank >> 1, pair_leader = rank & ~1u;
-  const bool leader = half == 0;
-  const int n0 = (blockIdx.x / (2 * S)) * BN;
-  const int m0 = blockIdx.y * 256 + half * 128;
-  const int total_kb = (K + C::BK - 1) / C::BK;
-  const int kb0 = z * kb_per_split;
-  const int nkb = max(0, min(kb_per_split, total_kb - kb0));
-
-  if (threadIdx.x == 0) {
-#pragma unroll 1
-    for (int s = 0; s < C::STAGES; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
-    }
-    ptx::mbar_init(accf, 1);
-    ptx::fence_barrier_init();
-  }
-  if (warp == 1) {
-    ptx::tmem_alloc2(tmem_slot, BN);
-    ptx::tmem_relinquish2();
-  }
-  if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tmA);
-    ptx::prefetch_tmap(&tmB);
-  }
-  ptx::tc_fence_before();
-  ptx::cluster_sync();
-  ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0 && nkb > 0) {
-      const uint64_t pa = ptx::make_policy(polA), pb = ptx::make_policy(polB);
-      const uint32_t full_leader0 = ptx::mapa_shared(ptx::smem_u32(&full[0]), pair_leader);
-#pragma unroll 1
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % C::STAGES;
-        const uint32_t ph = (i / C::STAGES) & 1;
-        ptx::mbar_wait(&empty[s], ph ^ 1);
-        if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * C::STAGE_BYTES);
-        const int kc = (kb0 + i) * C::BK;
-        if (tracing && i == 0) tr_ts[1] = ptx::globaltimer();
-        ptx::tma_load_3d_2sm(sA + s * C::A_BYTES, &tmA, full_leader0 + s * 8, kc, m0, az, pa);
-        ptx::tma_load_3d_2sm(sB + s * C::B_BYTES, &tmB, full_leader0 + s * 8, kc, n0 + half * (BN / 2), bz, pb);
-      }
-    }
-  } else if (warp == 1) {
-    if (leader && lane == 0 && nkb > 0) {
-      constexpr uint32_t idesc = ptx::idesc_f16_f32(256, BN);
-      const uint16_t mask = static_cast<uint16_t>(3u << pair_leader);
-#pragma unroll 1
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % C::STAGES;
-        const uint32_t ph = (i / C::STAGES) & 1;
-        ptx::mbar_wait(&full[s], ph);
-        ptx::tc_fence_after();
-        if (tracing && i == 0) tr_ts[2] = ptx::globaltimer();
-        const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
-        const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
-#pragma unroll
-        for (int k = 0; k < C::BK / 16; ++k)
-          ptx::mma_f16_2sm(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
-        ptx::mma_commit_2sm_mc(&empty[s], mask);
-      }
-      ptx::mma_commit_2sm_mc(accf, mask);
-    }
-  } else {
-    // stage this CTA's fp32 partial (128 rows x 256 cols) in its own shared memory
-    const int q = warp & 3;
-    const int rl = q * 32 + lane;
-    if (nkb > 0) {
-      ptx::mbar_wait(accf, 0);
-      ptx::tc_fence_after();
-    }
-    if (tracing && threadIdx.x == 64) tr_ts[3] = ptx::globaltimer();
-#pragma unroll 1
-    for (int c = 0; c < BN / 64; ++c) {
-      float v[64];
-      if (nkb > 0) {
-        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 64;
-        ptx::tmem_ld16(ta, v);
-        ptx::tmem_ld16(ta + 16, v + 16);
-        ptx::tmem_ld16(ta + 32, v + 32);
-        ptx::tmem_ld16(ta + 48, v + 48);
-        ptx::tmem_ld_wait();
-      } else {
-#pragma unroll
-        for (int i = 0; i < 64; ++i) v[i] = 0.f;
-      }
-      float4* dst = reinterpret_cast<float4*>(stage + rl * LDS + c * 64);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-    }
-  }
-  ptx::tc_fence_before();
-  ptx::cluster_sync();  // every partial of the cluster is staged
-  if (tracing && threadIdx.x == 0) tr_ts[4] = ptx::globaltimer();
-  if (warp >= 2) {
-    const int q = warp & 3;
-    const int rl = q * 32 + lane;
-    const int row = m0 + rl;
-    const uint32_t my = ptx::smem_u32(stage + rl * LDS + z * SLICE);
-#pragma unroll 1
-    for (int j = 0; j < SLICE / 64; ++j) {
-      float v[64];
-#pragma unroll
-      for (int i = 0; i < 64; ++i) v[i] = 0.f;
-#pragma unroll 1
-      for (int zz = 0; zz < S; ++zz) {
-        const uint32_t src = ptx::mapa_shared(my, 2 * zz + half) + j * 256;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float4 p = ptx::ld_dsmem_f4(src + 16 * i);
-          v[4 * i] += p.x;
-          v[4 * i + 1] += p.y;
-          v[4 * i + 2] += p.z;
-          v[4 * i + 3] += p.w;
-        }
-      }
-      const int col0 = n0 + z * SLICE + j * 64;
-      if (row < M && col0 < N) epi(row, col0, v);
-    }
-  }
-  ptx::cluster_sync();  // no CTA leaves while others still read its staging buffer
-  if (tracing && threadIdx.x == 0) {
-    tr_ts[5] = ptx::globaltimer();
-    trace_flush(tr_ts, EpiTag<Epi>::value);
-  }
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc2(tmem, BN);
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
-// gemm_tc1s_kernel: one CTA per 128 x 256 tile (full-rate M=128, N=256 tcgen05.mma) with the K
-// loop split S ways over the S CTAs of a cluster (cluster rank z = K split).  Used when 256-wide
-// tiles alone cannot fill the machine (the per-timestep GEMMs with N = h).  Each CTA writes its
-// fp32 partial to an L2-resident scratch; after the cluster barrier (release/acquire at cluster
-// scope orders those writes) CTA z sums columns [z*256/S, (z+1)*256/S) of its 128 rows over the S
-// partials in fixed order z' = 0..S-1 (deterministic) and runs the fused epilogue on that slice,
-// so the epilogue work stays spread over all S CTAs of the tile.
-template <int S, class Epi>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc1s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                     int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB,
+                     int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, int flags,
                      float* __restrict__ scratch, Epi epi) {
   constexpr int BN = 256;
   using C = TcCfg<BN>;
   constexpr int SLICE = BN / S;
-  static_assert(SLICE % 64 == 0, "slice is a whole number of epilogue chunks");
+  constexpr bool HALF_ROWS = Epi::kMinGroups <= SLICE / 32;  // can a thread take half a row?
+  constexpr int WIDTH = HALF_ROWS ? SLICE / 2 : SLICE;       // columns per thread
+  constexpr int PIECE = WIDTH > 64 ? 64 : WIDTH;             // columns per epilogue call
+  constexpr int NG = PIECE / 16;
+  static_assert(WIDTH % PIECE == 0 && NG >= Epi::kMinGroups, "epilogue granularity");
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* accf = empty + C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
-  __shared__ uint64_t tr_ts[6];
-  const bool tracing = g_trace != nullptr;
-  if (tracing && threadIdx.x == 0) {
-    for (int k = 1; k < 6; ++k) tr_ts[k] = 0;
-    tr_ts[0] = ptx::globaltimer();
-  }
-
+  const SmemLayout<C> L(smem_raw);
+  MLSTM_TRACE_BEGIN();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int z = (int)ptx::cluster_ctarank();
   const int tile_n = blockIdx.x / S;
@@ -588,150 +350,73 @@ __global__ void __launch_bounds__(192, 1)
   const int total_kb = (K + C::BK - 1) / C::BK;
   const int kb0 = z * kb_per_split;
   const int nkb = max(0, min(kb_per_split, total_kb - kb0));
-  float* stage_T = reinterpret_cast<float*>(smem);  // tile-epilogue staging (stages idle by then)
-  // this tile's S partials: scratch[(tile * S + z')][128][256]
   float* part = scratch + ((long)(blockIdx.y * (gridDim.x / S) + tile_n) * S) * (128L * BN);
-
-  if (threadIdx.x == 0) {
-#pragma unroll 1
-    for (int s = 0; s < C::STAGES; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
-    }
-    ptx::mbar_init(accf, 1);
-    ptx::fence_barrier_init();
-  }
-  if (warp == 1) {
-    ptx::tmem_alloc(tmem_slot, BN);
-    ptx::tmem_relinquish();
-  }
-  if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tmA);
-    ptx::prefetch_tmap(&tmB);
-  }
+  gemm_setup<C, false>(L, &tmA, &tmB, BN);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
+  const uint32_t tmem = *L.tmem_slot;
   if (warp == 0) {
-    if (lane == 0 && nkb > 0) {
-      const uint64_t pa = ptx::make_policy(polA), pb = ptx::make_policy(polB);
-#pragma unroll 1
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % C::STAGES;
-        const uint32_t ph = (i / C::STAGES) & 1;
-        ptx::mbar_wait(&empty[s], ph ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
-        const int kc = (kb0 + i) * C::BK;
-        if (tracing && i == 0) tr_ts[1] = ptx::globaltimer();
-        ptx::tma_load_3d(sA + s * C::A_BYTES, &tmA, &full[s], kc, m0, az, pa);
-        ptx::tma_load_3d(sB + s * C::B_BYTES, &tmB, &full[s], kc, n0, bz, pb);
-      }
-    }
+    if (lane == 0 && nkb > 0)
+      gemm_produce<C, false>(L, &tmA, &tmB, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true, 0,
+                             MLSTM_TRACE_SLOT(1));
   } else if (warp == 1) {
-    if (lane == 0 && nkb > 0) {
-      constexpr uint32_t idesc = ptx::idesc_f16_f32(C::BM, BN);
-#pragma unroll 1
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % C::STAGES;
-        const uint32_t ph = (i / C::STAGES) & 1;
-        ptx::mbar_wait(&full[s], ph);
-        ptx::tc_fence_after();
-        if (tracing && i == 0) tr_ts[2] = ptx::globaltimer();
-        const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
-        const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
-#pragma unroll
-        for (int k = 0; k < C::BK / 16; ++k)
-          ptx::mma_f16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
-        ptx::mma_commit(&empty[s]);
-      }
-      ptx::mma_commit(accf);
-    }
+    if (lane == 0 && nkb > 0) gemm_mma<C, false, BN>(L, tmem, nkb, 0, MLSTM_TRACE_SLOT(2));
   } else {
-    const int q = warp & 3;
+    const int q = warp & 3, grp = (warp - 2) >> 2;
     const int rl = q * 32 + lane;
-    if (nkb > 0) {
-      ptx::mbar_wait(accf, 0);
-      ptx::tc_fence_after();
-    }
-    if (tracing && threadIdx.x == 64) tr_ts[3] = ptx::globaltimer();
-    // partial layout [z][float4 column group (64)][row (128)]: lanes (= rows) write consecutive
-    // 16-byte vectors, fully coalesced; the reducer reads with the same mapping
+    epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
     float4* dst = reinterpret_cast<float4*>(part + (long)z * 128 * BN) + rl;
 #pragma unroll 1
-    for (int c = 0; c < BN / 64; ++c) {
+    for (int c = grp; c < BN / 64; c += 2) {
       float v[64];
-      if (nkb > 0) {
-        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 64;
-        ptx::tmem_ld16(ta, v);
-        ptx::tmem_ld16(ta + 16, v + 16);
-        ptx::tmem_ld16(ta + 32, v + 32);
-        ptx::tmem_ld16(ta + 48, v + 48);
-        ptx::tmem_ld_wait();
-      } else {
+      tmem_chunk(tmem, q, c, nkb > 0, v);
 #pragma unroll
-        for (int i = 0; i < 64; ++i) v[i] = 0.f;
-      }
-#pragma unroll
-      for (int i = 0; i < 16; ++i) dst[(c * 16 + i) * 128] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      for (int i = 0; i < 16; ++i)
+        dst[(c * 16 + i) * 128] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
     }
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();  // all S partials of the tile are written (cluster-scope release/acquire)
   if (tracing && threadIdx.x == 0) tr_ts[4] = ptx::globaltimer();
   if (warp >= 2) {
-    const int q = warp & 3;
-    const int rl = q * 32 + lane;
+    const int tid = threadIdx.x - 64;
+    const int rl = tid & 127, hh = tid >> 7;
     const int row = m0 + rl;
+    if (HALF_ROWS || hh == 0) {
 #pragma unroll 1
-    for (int j = 0; j < SLICE / 64; ++j) {
-      const int cl = z * SLICE + j * 64;
-      float v[64];
+      for (int j = 0; j < WIDTH / PIECE; ++j) {
+        const int cl = z * SLICE + (HALF_ROWS ? hh * WIDTH : 0) + j * PIECE;
+        float v[PIECE];
 #pragma unroll
-      for (int i = 0; i < 64; ++i) v[i] = 0.f;
+        for (int i = 0; i < PIECE; ++i) v[i] = 0.f;
 #pragma unroll 1
-      for (int zz = 0; zz < S; ++zz) {
-        const float4* src = reinterpret_cast<const float4*>(part + (long)zz * 128 * BN) + (cl / 4) * 128 + rl;
+        for (int zz = 0; zz < S; ++zz) {
+          const float4* src = reinterpret_cast<const float4*>(part + (long)zz * 128 * BN) + (cl / 4) * 128 + rl;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float4 p = __ldcg(src + i * 128);
-          v[4 * i] += p.x;
-          v[4 * i + 1] += p.y;
-          v[4 * i + 2] += p.z;
-          v[4 * i + 3] += p.w;
+          for (int i = 0; i < PIECE / 4; ++i) {
+            const float4 p = __ldcg(src + i * 128);
+            v[4 * i] += p.x;
+            v[4 * i + 1] += p.y;
+            v[4 * i + 2] += p.z;
+            v[4 * i + 3] += p.w;
+          }
         }
+        const int col0 = n0 + cl;
+        if (row < M && col0 < N) epi.template run<NG>(row, col0, v);
       }
-      const int col0 = n0 + cl;
-      if constexpr (IsTile<Epi>::value) {
-        float4* dst = reinterpret_cast<float4*>(stage_T + rl * (SLICE + 4) + j * 64);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-      } else {
-        if (row < M && col0 < N) epi(row, col0, v);
-      }
-    }
-    if constexpr (IsTile<Epi>::value) {
-      epi_bar_();
-      const int rows = min(128, M - m0);
-      const int c0 = n0 + z * SLICE;
-      if (rows > 0 && c0 < N)
-        epi.tile(stage_T, SLICE + 4, m0, c0, min(SLICE, N - c0), rows,
-                 reinterpret_cast<uint8_t*>(stage_T + 128 * (SLICE + 4)), (int)threadIdx.x - 64);
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (tracing && threadIdx.x == 0) {
-    tr_ts[5] = ptx::globaltimer();
-    trace_flush(tr_ts, EpiTag<Epi>::value);
-  }
+  MLSTM_TRACE_END();
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, BN);
   }
 }
 
+// ---------------------------------------------------------------------------------------------
 template <typename T>
 __device__ __forceinline__ float ld_as_float(const T* p) {
   return static_cast<float>(*p);
@@ -785,19 +470,7 @@ __global__ void __launch_bounds__(128)
     __syncthreads();
   }
   const int row = m0 + tid;
-  if constexpr (IsTile<Epi>::value) {
-    extern __shared__ float simt_dyn[];
-    float* T = simt_dyn;
-    float4* dst = reinterpret_cast<float4*>(T + tid * 68);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) dst[i] = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
-    __syncthreads();
-    const int rows = min(128, M - m0);
-    if (rows > 0 && n0 < N)
-      epi.tile(T, 68, m0, n0, min(64, N - n0), rows, reinterpret_cast<uint8_t*>(T + 128 * 68), tid);
-  } else {
-    if (row < M && n0 < N) epi(row, n0, acc);
-  }
+  if (row < M && n0 < N) epi.template run<4>(row, n0, acc);
 }
 
 }  // namespace mlstm

@@ -266,21 +266,24 @@ __device__ __forceinline__ long wgrad_col_canon(int mode, int c, int h) {
 
 template <typename S>
 struct EpiWgrad {
+  static constexpr int kMinGroups = 1;  // 16-column groups one call must cover
+  __device__ __forceinline__ void operator()(int row, int col0, float (&v)[64]) const { run<4>(row, col0, v); }
   Net<S> n;
   long off;
   int mode;
   int N;
-  __device__ __forceinline__ void operator()(int row, int col0, float (&v)[64]) const {
+  template <int NG>
+  __device__ __forceinline__ void run(int row, int col0, const float* v) const {
     if (mode == 2) {
       float* dst = n.Scan + (long)row * 5 * n.h;
 #pragma unroll
-      for (int i = 0; i < 64; ++i) dst[wgrad_col_canon(2, col0 + i, n.h)] = v[i];
+      for (int i = 0; i < 16 * NG; ++i) dst[wgrad_col_canon(2, col0 + i, n.h)] = v[i];
       return;
     }
     const long r = (mode == 1) ? canon_of_int(row, n.h) : row;
     S* dst = n.arena + off + r * N + col0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) st16(dst + 16 * q, v + 16 * q);
+    for (int q = 0; q < NG; ++q) st16(dst + 16 * q, v + 16 * q);
   }
 };
 

@@ -45,7 +45,8 @@ const char* kPhaseNames[NPH] = {"prep", "tab", "fwd_rec", "decoder", "ce", "dhde
 struct Opd {  // K-major operand view: [zdim][rows][K], element strides ld (row) and zstride
   const void* ptr;
   long rows, K, ld, zdim, zstride;
-  uint32_t pol = 0;  // L2 policy code for its TMA loads (ptx::make_policy)
+  uint32_t pol = 0;     // L2 policy code for its TMA loads (ptx::make_policy)
+  bool weight = false;  // a parameter copy: not written by any kernel of the step before the optimiser
 };
 constexpr uint32_t kPolFirst = 1u << 8;
 inline uint32_t pol_last(float frac) { return (2u << 8) | (uint32_t)(frac * 255.f + 0.5f); }
@@ -84,6 +85,7 @@ struct mlstm_ctx {
   int seg_splits = 1;
   float l2_wmh = 0.f, l2_wh = 0.f;  // evict_last fractions of the recurrent weights
   float* split_scratch = nullptr;
+  bool pdl = false;  // programmatic dependent launch of the GEMMs (MLSTM_PDL=1 enables; measured neutral)
   Net<__half> nh{};
   Net<float> nf{};
   ncclComm_t comm = nullptr;
@@ -277,6 +279,7 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   c->P = c->po.P;
   c->mixed = cfg->precision == MLSTM_MIXED;
   if (const char* v = getenv("MLSTM_L2_WMH")) c->l2_wmh = (float)atof(v);  // tuning knobs
+  if (const char* v = getenv("MLSTM_PDL")) c->pdl = v[0] != '0';
   if (const char* v = getenv("MLSTM_L2_WH")) c->l2_wh = (float)atof(v);
   const char* dbg = getenv("MLSTM_DEBUG_SIMT_GEMM");  // test instrument: mixed mode on the SIMT engine
   c->tc = c->mixed && !(dbg && dbg[0] == '1');
@@ -336,86 +339,60 @@ void count_launch(mlstm_ctx* c) {
   }
 }
 
-template <int BN, class Epi>
-cudaError_t launch_tc(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az, int bz, uint32_t pa, uint32_t pb,
-                      int splits, const Epi& epi) {
-  auto kern = gemm_tc_kernel<BN, Epi>;
-  const int smem = TcCfg<BN>::SMEM;
+// Launches one tcgen05 GEMM kernel: cluster dims for the pair / split engines and, when enabled,
+// programmatic dependent launch (the kernel waits on griddepcontrol before reading its inputs).
+template <typename Kern, typename... Args>
+cudaError_t launch_gemm(mlstm_ctx* c, Kern kern, dim3 grid, int smem, int cluster, Args... args) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  const int kb = (K + 63) / 64;
-  const int kbps = (kb + splits - 1) / splits;
-  dim3 grid((N + BN - 1) / BN, (M + 127) / 128, splits);
-  kern<<<grid, 192, smem, c->stream>>>(*ma, *mb, M, N, K, az, bz, kbps, pa, pb, epi);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (cluster > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = cluster;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (c->pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  e = cudaLaunchKernelEx(&cfg, kern, args...);
   count_launch(c);
-  return cudaGetLastError();
+  return e;
+}
+
+template <int BN, class Epi>
+cudaError_t launch_tc(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az, int bz,
+                      uint32_t pa, uint32_t pb, int flags, int splits, const Epi& epi) {
+  const int kb = (K + 63) / 64, kbps = (kb + splits - 1) / splits;
+  return launch_gemm(c, gemm_tc_kernel<BN, Epi>, dim3((N + BN - 1) / BN, (M + 127) / 128, splits), TcCfg<BN>::SMEM,
+                     1, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, flags, epi);
 }
 
 template <int S, class Epi>
 cudaError_t launch_tc1s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az,
-                        int bz, uint32_t pa, uint32_t pb, const Epi& epi) {
-  auto kern = gemm_tc1s_kernel<S, Epi>;
-  const int smem = TcCfg<256>::SMEM;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  const int kb = (K + 63) / 64;
-  const int kbps = (kb + S - 1) / S;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(S * ((N + 255) / 256), (M + 127) / 128, 1);
-  cfg.blockDim = dim3(192);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = c->stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = S;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, c->split_scratch, epi);
-  count_launch(c);
-  return e;
-}
-
-template <int S, class Epi>
-cudaError_t launch_tc2s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az,
-                        int bz, uint32_t pa, uint32_t pb, const Epi& epi) {
-  auto kern = gemm_tc2s_kernel<S, Epi>;
-  const int smem = Tc2Cfg<256>::SMEM;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  const int kb = (K + 63) / 64;
-  const int kbps = (kb + S - 1) / S;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * S * ((N + 255) / 256), (M + 255) / 256, 1);
-  cfg.blockDim = dim3(192);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = c->stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2 * S;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, epi);
-  count_launch(c);
-  return e;
+                        int bz, uint32_t pa, uint32_t pb, int flags, const Epi& epi) {
+  const int kb = (K + 63) / 64, kbps = (kb + S - 1) / S;
+  return launch_gemm(c, gemm_tc1s_kernel<S, Epi>, dim3(S * ((N + 255) / 256), (M + 127) / 128, 1), TcCfg<256>::SMEM,
+                     S, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, flags, c->split_scratch, epi);
 }
 
 template <int BN, class Epi>
 cudaError_t launch_tc2(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az,
-                       int bz, uint32_t pa, uint32_t pb, int splits, const Epi& epi) {
-  auto kern = gemm_tc2_kernel<BN, Epi>;
-  const int smem = Tc2Cfg<BN>::SMEM;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  const int kb = (K + 63) / 64;
-  const int kbps = (kb + splits - 1) / splits;
-  dim3 grid(2 * ((N + BN - 1) / BN), (M + 255) / 256, splits);
-  kern<<<grid, 192, smem, c->stream>>>(*ma, *mb, M, N, K, az, bz, kbps, pa, pb, epi);
-  count_launch(c);
-  return cudaGetLastError();
+                       int bz, uint32_t pa, uint32_t pb, int flags, int splits, const Epi& epi) {
+  const int kb = (K + 63) / 64, kbps = (kb + splits - 1) / splits;
+  return launch_gemm(c, gemm_tc2_kernel<BN, Epi>, dim3(2 * ((N + BN - 1) / BN), (M + 255) / 256, splits),
+                     Tc2Cfg<BN>::SMEM, 2, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, flags, epi);
 }
 
 // D[M x N] = A[az] . B[bz]^T, fused epilogue.  `splits` > 1 only with a partial epilogue.
@@ -431,23 +408,21 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
       return MLSTM_ECUDA;
     }
     cudaError_t e;
+    const int gflags = B.weight ? kGemmStaticB : 0;
     if (p.cluster) {
-      e = p.splits == 2 ? launch_tc1s<2>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, epi)
-                        : launch_tc1s<4>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, epi);
-    } else if (p.pair && p.splits > 1) {
-      e = p.splits == 2 ? launch_tc2s<2>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, epi)
-                        : launch_tc2s<4>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, epi);
+      e = p.splits == 2 ? launch_tc1s<2>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, epi)
+                        : launch_tc1s<4>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, epi);
     } else if (p.pair) {
       switch (p.bn) {
-        case 256: e = launch_tc2<256>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, p.splits, epi); break;
-        case 128: e = launch_tc2<128>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, p.splits, epi); break;
-        default: e = launch_tc2<64>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, p.splits, epi); break;
+        case 256: e = launch_tc2<256>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, epi); break;
+        case 128: e = launch_tc2<128>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, epi); break;
+        default: e = launch_tc2<64>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, epi); break;
       }
     } else {
       switch (p.bn) {
-        case 256: e = launch_tc<256>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, p.splits, epi); break;
-        case 128: e = launch_tc<128>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, p.splits, epi); break;
-        default: e = launch_tc<64>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, p.splits, epi); break;
+        case 256: e = launch_tc<256>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, epi); break;
+        case 128: e = launch_tc<128>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, epi); break;
+        default: e = launch_tc<64>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, epi); break;
       }
     }
     CUDA_OR_FAIL(c, e);
@@ -458,12 +433,7 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
   const S* b = static_cast<const S*>(B.ptr) + (long)bz * B.zstride;
   const int kps = (int)rup((K + p.splits - 1) / p.splits, 32);
   dim3 grid((N + 63) / 64, (M + 127) / 128, p.splits);
-  int dsm = 0;
-  if constexpr (IsTile<Epi>::value) {
-    dsm = tile_smem_bytes(64);
-    CUDA_OR_FAIL(c, cudaFuncSetAttribute(gemm_simt_kernel<S, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm));
-  }
-  gemm_simt_kernel<S, Epi><<<grid, 128, dsm, c->stream>>>(a, A.ld, b, B.ld, M, N, K, kps, epi);
+  gemm_simt_kernel<S, Epi><<<grid, 128, 0, c->stream>>>(a, A.ld, b, B.ld, M, N, K, kps, epi);
   count_launch(c);
   CUDA_OR_FAIL(c, cudaGetLastError());
   return MLSTM_OK;
@@ -529,16 +499,16 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   phase(c, PH_TAB);
   {
     Opd A{n.E_w, 256, e, e, 1, 256L * e};
-    Opd Bo{n.Wcat_w, 5L * h, e, e, 1, 5L * h * e};
+    Opd Bo{n.Wcat_w, 5L * h, e, e, 1, 5L * h * e, 0, true};
     RET_IF(gemm<S>(c, A, 0, Bo, 0, 256, 5 * h, e, plan_gemm(c->tc, 256, 5 * h, e, false), EpiTab<S>{n}));
   }
   phase(c, PH_FWD);
   // L2 policy: the recurrent weights are re-read every timestep -- keep W_mh and a fraction of
   // W_h resident (evict_last); the activations are read once (evict_first).
   const Opd Hprev{n.Hrm, B, h, h, T + 1, (long)B * h, kPolFirst};
-  const Opd Wmh{n.Wmh_w, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh)};
+  const Opd Wmh{n.Wmh_w, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh), true};
   const Opd Msc{n.Mscr, B, h, h, 1, (long)B * h, kPolFirst};
-  const Opd Wh{n.Wh_w, 4L * h, h, h, 1, 4L * h * h, pol_last(c->l2_wh)};
+  const Opd Wh{n.Wh_w, 4L * h, h, h, 1, 4L * h * h, pol_last(c->l2_wh), true};
   const Plan p1 = plan_gemm(c->tc, B, h, h, false), p2 = plan_gemm(c->tc, B, 4 * h, h, false);
   for (int t = 0; t < T; ++t) {
     RET_IF(gemm<S>(c, Hprev, t, Wmh, 0, B, h, h, p1, EpiF1<S>{n, t}));
@@ -547,7 +517,7 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   phase(c, PH_DEC);
   {
     Opd A{n.Hrm + (long)B * h, (long)T * B, h, h, 1, (long)T * B * h};
-    Opd Bo{n.Wdec_w, 256, h, h, 1, 256L * h};
+    Opd Bo{n.Wdec_w, 256, h, h, 1, 256L * h, 0, true};
     RET_IF(gemm<S>(c, A, 0, Bo, 0, T * B, 256, h, plan_gemm(c->tc, (long)T * B, 256, h, false), EpiY<S>{n}));
   }
   return MLSTM_OK;
@@ -570,16 +540,16 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
   phase(c, PH_DHDEC);
   {
     Opd A{n.dY, (long)T * B, 256, 256, 1, (long)T * B * 256};
-    Opd Bo{n.WdecT, h, 256, 256, 1, 256L * h};
+    Opd Bo{n.WdecT, h, 256, 256, 1, 256L * h, 0, true};
     RET_IF(gemm<S>(c, A, 0, Bo, 0, T * B, h, 256, plan_gemm(c->tc, (long)T * B, h, 256, false), EpiDHdec<S>{n}));
   }
   phase(c, PH_BWD);
   LAUNCH(c, (gate_bwd_last_kernel<S><<<grid_for((long)B * h / 16), 256, 0, c->stream>>>(n)));
   {
     const Opd dZ{n.dZscr, B, 4L * h, 4L * h, 1, 4L * B * h, kPolFirst};
-    const Opd WhT{n.WhT, h, 4L * h, 4L * h, 1, 4L * h * h, pol_last(c->l2_wh)};
+    const Opd WhT{n.WhT, h, 4L * h, 4L * h, 1, 4L * h * h, pol_last(c->l2_wh), true};
     const Opd dA{n.dAscr, B, h, h, 1, (long)B * h, kPolFirst};
-    const Opd WmhT{n.WmhT, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh)};
+    const Opd WmhT{n.WmhT, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh), true};
     const Plan p1 = plan_gemm(c->tc, B, h, 4 * h, false), p2 = plan_gemm(c->tc, B, h, h, false);
     for (int t = T - 1; t >= 0; --t) {
       RET_IF(gemm<S>(c, dZ, 0, WhT, 0, B, h, 4 * h, p1, EpiB1<S>{n, t}));
@@ -1167,7 +1137,7 @@ int32_t mlstm_launches_per_step(mlstm_ctx* c) {
 }
 
 mlstm_status mlstm_gemm_bench(int engine, int M, int N, int K, int bn, int iters, double* ms) {
-  if (!ms || M <= 0 || N <= 0 || K <= 0 || iters <= 0 || engine < 1 || engine > 4 ||
+  if (!ms || M <= 0 || N <= 0 || K <= 0 || iters <= 0 || engine < 1 || engine > 3 ||
       (bn != 0 && bn != 64 && bn != 128 && bn != 256) || N % 64 || K % 8)
     return fail(MLSTM_EINVAL, "bad gemm_bench arguments");
   if (!get_encoder()) return fail(MLSTM_ECUDA, "cuTensorMapEncodeTiled unavailable");
@@ -1192,14 +1162,9 @@ mlstm_status mlstm_gemm_bench(int engine, int M, int N, int K, int bn, int iters
   const long nA = (long)M * K, nB = (long)N * K;
   cudaMemset(A, 0x3c, 2L * M * K);  // operand values do not matter for timing
   cudaMemset(B, 0x3c, 2L * N * K);
-  Opd oa{A, M, K, K, 1, nA}, ob{B, N, K, K, 1, nB};
+  Opd oa{A, M, K, K, 1, nA}, ob{B, N, K, K, 1, nB, 0, true};
   Plan p = plan_gemm(true, M, N, K, false);
-  if (engine == 4) {  // CTA pairs, K split 2 ways over a cluster of 4
-    p.pair = true;
-    p.cluster = false;
-    p.splits = 2;
-    p.bn = 256;
-  } else if (engine != 3) {
+  if (engine != 3) {
     p.cluster = false;
     p.pair = engine == 2;
     p.splits = 1;
