@@ -197,6 +197,25 @@ __device__ __forceinline__ void tmem_chunk(uint32_t tmem, int q, int c, bool hav
   }
 }
 
+// L2 prefetch job for the NEXT kernel's weight operand: the first `bytes` bytes of it (whole
+// contiguous N-tile row blocks), split evenly over this grid's CTAs, one bulk prefetch per CTA,
+// issued by the producer thread after its own loads (the TMA unit is a FIFO: queued ahead of them
+// the prefetch would delay this kernel's mainloop).
+struct PrefetchJob {
+  const uint8_t* base;
+  long bytes;
+};
+__device__ __forceinline__ void l2_prefetch(const PrefetchJob& pj) {
+  if (pj.bytes <= 0) return;
+  const long G = (long)gridDim.x * gridDim.y * gridDim.z;
+  const long lin = blockIdx.x + (long)gridDim.x * (blockIdx.y + (long)gridDim.y * blockIdx.z);
+  const long chunk = ((pj.bytes + G - 1) / G + 15) / 16 * 16;
+  const long off = lin * chunk;
+  if (off >= pj.bytes) return;
+  const long n = min(chunk, pj.bytes - off);
+  ptx::bulk_prefetch_l2(pj.base + off, (uint32_t)n, ptx::policy_evict_last());
+}
+
 // Epilogue warps' common start: wait for the accumulator, then for the preceding grid (inputs
 // of the fused epilogue), and let the next kernel's prologue start.
 __device__ __forceinline__ void epi_begin(uint64_t* accf, bool have, uint64_t* trace_slot) {
@@ -228,7 +247,7 @@ template <int BN, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                    int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, int flags,
-                   Epi epi) {
+                   PrefetchJob pj, Epi epi) {
   using C = TcCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   const SmemLayout<C> L(smem_raw);
@@ -244,9 +263,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *L.tmem_slot;
   if (warp == 0) {
-    if (lane == 0 && nkb > 0)
-      gemm_produce<C, false>(L, &tmA, &tmB, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true, 0,
-                             MLSTM_TRACE_SLOT(1));
+    if (lane == 0) {
+      if (nkb > 0)
+        gemm_produce<C, false>(L, &tmA, &tmB, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true, 0,
+                               MLSTM_TRACE_SLOT(1));
+      l2_prefetch(pj);
+    }
   } else if (warp == 1) {
     if (lane == 0 && nkb > 0) gemm_mma<C, false, BN>(L, tmem, nkb, 0, MLSTM_TRACE_SLOT(2));
   } else {
@@ -275,7 +297,7 @@ template <int BN, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                     int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, int flags,
-                    Epi epi) {
+                    PrefetchJob pj, Epi epi) {
   using C = Tc2Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   const SmemLayout<C> L(smem_raw);
@@ -294,9 +316,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *L.tmem_slot;
   if (warp == 0) {
-    if (lane == 0 && nkb > 0)
-      gemm_produce<C, true>(L, &tmA, &tmB, nkb, kb0, m0, n0 + rank * (BN / 2), az, bz, polA, polB, flags, leader,
-                            ptx::mapa_shared(ptx::smem_u32(&L.full[0]), 0), MLSTM_TRACE_SLOT(1));
+    if (lane == 0) {
+      if (nkb > 0)
+        gemm_produce<C, true>(L, &tmA, &tmB, nkb, kb0, m0, n0 + rank * (BN / 2), az, bz, polA, polB, flags,
+                              leader, ptx::mapa_shared(ptx::smem_u32(&L.full[0]), 0), MLSTM_TRACE_SLOT(1));
+      l2_prefetch(pj);
+    }
   } else if (warp == 1) {
     if (leader && lane == 0 && nkb > 0) gemm_mma<C, true, BN>(L, tmem, nkb, 0x3, MLSTM_TRACE_SLOT(2));
   } else {
@@ -331,7 +356,8 @@ template <int S, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc1s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
                      int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, int flags,
-                     float* __restrict__ scratch, Epi epi) {
+                     PrefetchJob pj, float* __restrict__ scratch,
+                     Epi epi) {
   constexpr int BN = 256;
   using C = TcCfg<BN>;
   constexpr int SLICE = BN / S;
@@ -357,9 +383,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *L.tmem_slot;
   if (warp == 0) {
-    if (lane == 0 && nkb > 0)
-      gemm_produce<C, false>(L, &tmA, &tmB, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true, 0,
-                             MLSTM_TRACE_SLOT(1));
+    if (lane == 0) {
+      if (nkb > 0)
+        gemm_produce<C, false>(L, &tmA, &tmB, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true, 0,
+                               MLSTM_TRACE_SLOT(1));
+      l2_prefetch(pj);
+    }
   } else if (warp == 1) {
     if (lane == 0 && nkb > 0) gemm_mma<C, false, BN>(L, tmem, nkb, 0, MLSTM_TRACE_SLOT(2));
   } else {

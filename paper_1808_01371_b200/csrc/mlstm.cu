@@ -85,7 +85,9 @@ struct mlstm_ctx {
   int seg_splits = 1;
   float l2_wmh = 0.f, l2_wh = 0.f;  // evict_last fractions of the recurrent weights
   float* split_scratch = nullptr;
-  bool pdl = false;  // programmatic dependent launch of the GEMMs (MLSTM_PDL=1 enables; measured neutral)
+  bool pdl = false;                   // programmatic dependent launch of the GEMMs (MLSTM_PDL=1; neutral)
+  float pf_fwd = 0.f, pf_bwd = 0.f;   // L2 prefetch of the next W_h / W_h^T (MLSTM_PF_FWD/BWD; neutral,
+                                      // profiles/r01_l2_prefetch.log)
   Net<__half> nh{};
   Net<float> nf{};
   ncclComm_t comm = nullptr;
@@ -280,6 +282,8 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   c->mixed = cfg->precision == MLSTM_MIXED;
   if (const char* v = getenv("MLSTM_L2_WMH")) c->l2_wmh = (float)atof(v);  // tuning knobs
   if (const char* v = getenv("MLSTM_PDL")) c->pdl = v[0] != '0';
+  if (const char* v = getenv("MLSTM_PF_FWD")) c->pf_fwd = (float)atof(v);
+  if (const char* v = getenv("MLSTM_PF_BWD")) c->pf_bwd = (float)atof(v);
   if (const char* v = getenv("MLSTM_L2_WH")) c->l2_wh = (float)atof(v);
   const char* dbg = getenv("MLSTM_DEBUG_SIMT_GEMM");  // test instrument: mixed mode on the SIMT engine
   c->tc = c->mixed && !(dbg && dbg[0] == '1');
@@ -373,32 +377,40 @@ cudaError_t launch_gemm(mlstm_ctx* c, Kern kern, dim3 grid, int smem, int cluste
 
 template <int BN, class Epi>
 cudaError_t launch_tc(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az, int bz,
-                      uint32_t pa, uint32_t pb, int flags, int splits, const Epi& epi) {
+                      uint32_t pa, uint32_t pb, int flags, int splits, PrefetchJob pj,
+                      const Epi& epi) {
   const int kb = (K + 63) / 64, kbps = (kb + splits - 1) / splits;
   return launch_gemm(c, gemm_tc_kernel<BN, Epi>, dim3((N + BN - 1) / BN, (M + 127) / 128, splits), TcCfg<BN>::SMEM,
-                     1, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, flags, epi);
+                     1, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, flags, pj, epi);
 }
 
 template <int S, class Epi>
 cudaError_t launch_tc1s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az,
-                        int bz, uint32_t pa, uint32_t pb, int flags, const Epi& epi) {
+                        int bz, uint32_t pa, uint32_t pb, int flags, PrefetchJob pj,
+                        const Epi& epi) {
   const int kb = (K + 63) / 64, kbps = (kb + S - 1) / S;
   return launch_gemm(c, gemm_tc1s_kernel<S, Epi>, dim3(S * ((N + 255) / 256), (M + 127) / 128, 1), TcCfg<256>::SMEM,
-                     S, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, flags, c->split_scratch, epi);
+                     S, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, flags, pj, c->split_scratch, epi);
 }
 
 template <int BN, class Epi>
 cudaError_t launch_tc2(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az,
-                       int bz, uint32_t pa, uint32_t pb, int flags, int splits, const Epi& epi) {
+                       int bz, uint32_t pa, uint32_t pb, int flags, int splits, PrefetchJob pj,
+                       const Epi& epi) {
   const int kb = (K + 63) / 64, kbps = (kb + splits - 1) / splits;
   return launch_gemm(c, gemm_tc2_kernel<BN, Epi>, dim3(2 * ((N + BN - 1) / BN), (M + 255) / 256, splits),
-                     Tc2Cfg<BN>::SMEM, 2, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, flags, epi);
+                     Tc2Cfg<BN>::SMEM, 2, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, flags, pj, epi);
 }
 
 // D[M x N] = A[az] . B[bz]^T, fused epilogue.  `splits` > 1 only with a partial epilogue.
+// Optional L2 prefetch of the next GEMM's weight operand (see l2_prefetch in gemm.cuh).
+struct Prefetch {
+  PrefetchJob job{nullptr, 0};
+};
+
 template <typename S, class Epi>
 mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int M, int N, int K, Plan p,
-                  const Epi& epi) {
+                  const Epi& epi, const Prefetch& pf = Prefetch{}) {
   if constexpr (std::is_same<S, __half>::value) {
     if (c->tc) {
     const CUtensorMap* ma = get_map(c, A, 128);
@@ -409,20 +421,21 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
     }
     cudaError_t e;
     const int gflags = B.weight ? kGemmStaticB : 0;
+    const PrefetchJob pj = pf.job;
     if (p.cluster) {
-      e = p.splits == 2 ? launch_tc1s<2>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, epi)
-                        : launch_tc1s<4>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, epi);
+      e = p.splits == 2 ? launch_tc1s<2>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, pj, epi)
+                        : launch_tc1s<4>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, pj, epi);
     } else if (p.pair) {
       switch (p.bn) {
-        case 256: e = launch_tc2<256>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, epi); break;
-        case 128: e = launch_tc2<128>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, epi); break;
-        default: e = launch_tc2<64>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, epi); break;
+        case 256: e = launch_tc2<256>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
+        case 128: e = launch_tc2<128>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
+        default: e = launch_tc2<64>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
       }
     } else {
       switch (p.bn) {
-        case 256: e = launch_tc<256>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, epi); break;
-        case 128: e = launch_tc<128>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, epi); break;
-        default: e = launch_tc<64>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, epi); break;
+        case 256: e = launch_tc<256>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
+        case 128: e = launch_tc<128>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
+        default: e = launch_tc<64>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
       }
     }
     CUDA_OR_FAIL(c, e);
@@ -510,8 +523,12 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   const Opd Msc{n.Mscr, B, h, h, 1, (long)B * h, kPolFirst};
   const Opd Wh{n.Wh_w, 4L * h, h, h, 1, 4L * h * h, pol_last(c->l2_wh), true};
   const Plan p1 = plan_gemm(c->tc, B, h, h, false), p2 = plan_gemm(c->tc, B, 4 * h, h, false);
+  // F1 (light on HBM) prefetches into L2 the first k-blocks of every W_h tile F2 will stream
+  Prefetch pf1;
+  if (c->pf_fwd > 0 && c->tc)
+    pf1.job = PrefetchJob{reinterpret_cast<const uint8_t*>(n.Wh_w), (long)(c->pf_fwd * 8.0 * h * h) / 16 * 16};
   for (int t = 0; t < T; ++t) {
-    RET_IF(gemm<S>(c, Hprev, t, Wmh, 0, B, h, h, p1, EpiF1<S>{n, t}));
+    RET_IF(gemm<S>(c, Hprev, t, Wmh, 0, B, h, h, p1, EpiF1<S>{n, t}, pf1));
     RET_IF(gemm<S>(c, Msc, 0, Wh, 0, B, 4 * h, h, p2, EpiF2<S>{n, t}));
   }
   phase(c, PH_DEC);
@@ -551,9 +568,13 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
     const Opd dA{n.dAscr, B, h, h, 1, (long)B * h, kPolFirst};
     const Opd WmhT{n.WmhT, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh), true};
     const Plan p1 = plan_gemm(c->tc, B, h, 4 * h, false), p2 = plan_gemm(c->tc, B, h, h, false);
+    // B2 prefetches into L2 the first k-blocks (of each K split) of the W_h^T tiles B1 streams next
+    Prefetch pf2;
+    if (c->pf_bwd > 0 && c->tc)
+      pf2.job = PrefetchJob{reinterpret_cast<const uint8_t*>(n.WhT), (long)(c->pf_bwd * 8.0 * h * h) / 16 * 16};
     for (int t = T - 1; t >= 0; --t) {
       RET_IF(gemm<S>(c, dZ, 0, WhT, 0, B, h, 4 * h, p1, EpiB1<S>{n, t}));
-      if (t > 0) RET_IF(gemm<S>(c, dA, 0, WmhT, 0, B, h, h, p2, EpiB2<S>{n, t - 1}));
+      if (t > 0) RET_IF(gemm<S>(c, dA, 0, WmhT, 0, B, h, h, p2, EpiB2<S>{n, t - 1}, pf2));
     }
   }
   phase(c, PH_WGRAD);

@@ -1,0 +1,46 @@
+"""Data parallel on real GPUs (NCCL over NVLink): N ranks through the C ABI against the fp64 oracle
+on the concatenated rows (S:405 serial equivalence), with bitwise replica consistency (every
+worker applies the identical update).  Skipped unless >= 2 GPUs are visible."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from oracle import mlstm_oracle as O
+from synth import bytestream
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("world", [2] + ([4] if NGPU >= 4 else []))
+def test_dp_matches_oracle_on_concatenated_rows(tmp_path, world):
+    h, e, B, T, steps = 128, 64, 130, 8, 3
+    out = str(tmp_path / "dp")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={29600 + world}", os.path.join(HERE, "dp_worker.py"),
+           out, str(h), str(e), str(B), str(T), str(steps)]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    R = [np.load(f"{out}.rank{r}.npz") for r in range(world)]
+    # replicas: bitwise identical masters and identical global losses on every rank
+    for r in range(1, world):
+        assert np.array_equal(R[0]["theta"], R[r]["theta"])
+        assert np.array_equal(R[0]["losses"], R[r]["losses"])
+    # step 0 against the oracle on all B*world rows (global mean loss and gradient)
+    theta0 = R[0]["theta0"].astype(np.float64)
+    by = bytestream.window(np.arange(B * world), 0, T)
+    P = O.unflatten(theta0, h, e)
+    z = np.zeros((B * world, h))
+    loss_sum, g_ref, _, _ = O.loss_and_grads(P, by, z, z)
+    loss_ref = loss_sum / (B * world * T)
+    assert abs(R[0]["losses"][0] - loss_ref) <= 5e-3 * loss_ref
+    G = O.unflatten(R[0]["grads0"].astype(np.float64), h, e)
+    for n in O.PARAM_NAMES:
+        a, b = G[n].ravel(), g_ref[n].ravel()
+        assert float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b))) >= 0.999, n
