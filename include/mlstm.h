@@ -184,10 +184,11 @@ mlstm_status mlstm_gemm_bench(int engine, int M, int N, int K, int bn, int iters
 
 /* Diagnostics: intra-kernel timeline of the tensor-core GEMM kernels.  mlstm_trace_enable(cap)
  * installs a device buffer of cap records (0 disables); every GEMM CTA then appends one record of
- * 8 uint64: {epilogue tag, cta index, t_start, t_first_tma, t_first_data, t_acc_ready, t_reduced,
- * t_end} (%globaltimer ns; 0 where not applicable).  Tags: 1 F1, 2 F2, 3 B1, 4 B2, 5 decoder,
+ * 12 uint64: {epilogue tag, cta index, t_start, t_first_tma, t_first_data, t_acc_ready, t_reduced,
+ * t_end, t_partial_reduce_done, t_tile_begin, t_tile_end, 0} (%globaltimer ns; 0 where not
+ * applicable).  Tags: 1 F1, 2 F2, 3 B1, 4 B2, 5 decoder,
  * 6 dH_dec, 7 input table, 8 weight gradient, 9 split partial.  mlstm_trace_read copies up to
- * `capacity` records (8*capacity uint64) and resets the count. */
+ * `capacity` records (12*capacity uint64) and resets the count. */
 mlstm_status mlstm_trace_enable(int capacity);
 mlstm_status mlstm_trace_read(uint64_t* out, int capacity, int* n);
 

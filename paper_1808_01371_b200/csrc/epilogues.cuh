@@ -209,6 +209,95 @@ struct EpiB1 {
   }
 };
 
+
+// Cooperative tile form of the gate backward (used by the split-K engine, whose reduced fp32 tile
+// T[rows][U] (row stride ldt, columns = hidden units n0..n0+U) sits in shared memory).  The row-
+// per-thread form touches 32 cache lines per warp instruction, which makes the L1 wavefront rate,
+// not DRAM, the bound; here 16 lanes x 4 units cover 64 units of one row (two rows per warp
+// instruction, 8/16-byte vectors) and each thread batches RB rows' loads before any store.  The
+// transposed dZ stash goes through shared memory Zs[gate*U + unit][row] and leaves with lanes
+// along rows (8-byte stores of 4 consecutive batch rows).  256 threads, tid in [0, 256).
+__device__ __forceinline__ void epi_bar256() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+template <typename S>
+__device__ __forceinline__ void b2_tile(const Net<S>& n, int s, const float* T, int ldt, int m0, int n0, int U,
+                                        int rows, uint8_t* sm, int tid) {
+  constexpr int RB = 4;
+  const int h = n.h, ng = U / 4, rpi = 256 / ng;
+  const int ug = tid % ng, rr = tid / ng;
+  const int u0 = 4 * ug, j = n0 + u0;
+  const long gcol = (long)(j >> 4) * 64 + (j & 15);  // internal column of gate i of unit j
+  // Zs[row][gate * U + unit], row stride 4U + 2 elements: pass-1 writes are contiguous vectors,
+  // pass-2 reads (lanes on consecutive rows) hit distinct banks.
+  const int ldz = 4 * U + 2;
+  S* Zs = reinterpret_cast<S*>(sm);
+  if (rr < rpi) {
+    for (int rb = rr; rb < rows; rb += rpi * RB) {
+      float4 dh[RB], gi[RB], gf[RB], go[RB], gu[RB], c[RB], cp[RB], dcn[RB];
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const int r = min(rb + k * rpi, rows - 1);
+        const long row = (long)s * n.B + m0 + r;
+        const float4 t4 = *reinterpret_cast<const float4*>(T + r * ldt + u0);
+        const float4 d4 = ld4(n.dHdec + row * h + j);
+        dh[k] = make_float4(t4.x + d4.x, t4.y + d4.y, t4.z + d4.z, t4.w + d4.w);
+        const S* g = n.Gates + row * 4 * h + gcol;
+        gi[k] = ld4(g);
+        gf[k] = ld4(g + 16);
+        go[k] = ld4(g + 32);
+        gu[k] = ld4(g + 48);
+        c[k] = ld4(n.Crm + (row + n.B) * h + j);
+        cp[k] = ld4(n.Crm + row * h + j);
+        dcn[k] = ld4(n.dC + (long)(m0 + r) * h + j);
+
+      }
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const int r = rb + k * rpi;
+        if (r >= rows) break;
+        float dzi[4], dzf[4], dzo[4], dzu[4], dcw[4];
+        const float* DH = &dh[k].x;
+        const float *I = &gi[k].x, *F = &gf[k].x, *O = &go[k].x, *UU = &gu[k].x;
+        const float *CC = &c[k].x, *CP = &cp[k].x, *DC = &dcn[k].x;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float kk = act_tanh<S>(CC[i]);
+          dzo[i] = DH[i] * kk * O[i] * (1.f - O[i]);
+          const float dc = DC[i] + DH[i] * O[i] * (1.f - kk * kk);
+          dzi[i] = dc * UU[i] * I[i] * (1.f - I[i]);
+          dzf[i] = dc * CP[i] * F[i] * (1.f - F[i]);
+          dzu[i] = dc * I[i] * (1.f - UU[i] * UU[i]);
+          dcw[i] = dc * F[i];
+        }
+        const long b = m0 + r;
+        st4(n.dC + b * h + j, make_float4(dcw[0], dcw[1], dcw[2], dcw[3]));
+        S* zr = n.dZscr + b * 4 * h + gcol;
+        st4(zr, make_float4(dzi[0], dzi[1], dzi[2], dzi[3]));
+        st4(zr + 16, make_float4(dzf[0], dzf[1], dzf[2], dzf[3]));
+        st4(zr + 32, make_float4(dzo[0], dzo[1], dzo[2], dzo[3]));
+        st4(zr + 48, make_float4(dzu[0], dzu[1], dzu[2], dzu[3]));
+        S* zs = Zs + r * ldz + u0;
+        st4s(zs, make_float4(dzi[0], dzi[1], dzi[2], dzi[3]));
+        st4s(zs + U, make_float4(dzf[0], dzf[1], dzf[2], dzf[3]));
+        st4s(zs + 2 * U, make_float4(dzo[0], dzo[1], dzo[2], dzo[3]));
+        st4s(zs + 3 * U, make_float4(dzu[0], dzu[1], dzu[2], dzu[3]));
+      }
+    }
+  }
+  epi_bar256();
+  // pass 2: dGT[h + gate-unit row][kcol(s, b)]: lanes on consecutive batch rows (2-byte stores,
+  // 64 contiguous bytes per warp instruction)
+  const int warp = tid >> 5, lane = tid & 31;
+  const long kc0 = n.kcol(s, m0);
+  for (int g_u = warp; g_u < 4 * U; g_u += 8) {
+    const int g = g_u / U, u = g_u - g * U;
+    S* dst = n.dGT + ((long)h + int_row(g, n0 + u)) * n.ldK + kc0;
+#pragma unroll
+    for (int r = lane; r < 128; r += 32)
+      if (r < rows) dst[r] = Zs[r * ldz + g_u];
+  }
+}
+
 // (c-1) backward GEMM 2, dH_rec = dA_t W_mh, fused with the gate backward of step s = t-1.
 template <typename S>
 struct EpiB2 {
@@ -216,6 +305,11 @@ struct EpiB2 {
   __device__ __forceinline__ void operator()(int row, int col0, float (&v)[64]) const { run<4>(row, col0, v); }
   Net<S> n;
   int s;
+  static constexpr bool kTile = true;  // the split-K engine calls tile()
+  __device__ __forceinline__ void tile(const float* T, int ldt, int m0, int n0, int U, int rows, uint8_t* sm,
+                                       int tid) const {
+    b2_tile(n, s, T, ldt, m0, n0, U, rows, sm, tid);
+  }
   template <int NG>
   __device__ __forceinline__ void run(int b, int col0, const float* v) const {
     const float* dhd = n.dHdec + ((long)s * n.B + b) * n.h + col0;

@@ -27,7 +27,7 @@ constexpr int kGemmStaticB = 1;  // B operand is a weight untouched by the prece
 // ---- optional intra-kernel timeline (mlstm_trace_enable): one record per CTA,
 // {tag, cta, t_start, t_first_tma, t_first_full, t_acc_ready, t_reduced, t_end} in ns.
 struct TraceRec {
-  uint64_t v[8];
+  uint64_t v[12];
 };
 __device__ TraceRec* g_trace = nullptr;
 __device__ unsigned int g_trace_n = 0;
@@ -40,12 +40,20 @@ __device__ __forceinline__ void trace_flush(const uint64_t* ts, int tag) {
   TraceRec r;
   r.v[0] = (uint64_t)tag;
   r.v[1] = blockIdx.x + (uint64_t)gridDim.x * (blockIdx.y + (uint64_t)gridDim.y * blockIdx.z);
-  for (int k = 0; k < 6; ++k) r.v[2 + k] = ts[k];
+  for (int k = 0; k < 10; ++k) r.v[2 + k] = ts[k];
   tr[i] = r;
 }
 template <class Epi>
 struct EpiTag {
   static constexpr int value = 0;
+};
+template <class E, class = void>
+struct HasTile {  // epilogue with a cooperative tile() form (used by the split-K engine)
+  static constexpr bool value = false;
+};
+template <class E>
+struct HasTile<E, decltype(void(E::kTile))> {
+  static constexpr bool value = E::kTile;
 };
 
 template <int BN>
@@ -197,23 +205,26 @@ __device__ __forceinline__ void tmem_chunk(uint32_t tmem, int q, int c, bool hav
   }
 }
 
-// L2 prefetch job for the NEXT kernel's weight operand: the first `bytes` bytes of it (whole
-// contiguous N-tile row blocks), split evenly over this grid's CTAs, one bulk prefetch per CTA,
-// issued by the producer thread after its own loads (the TMA unit is a FIFO: queued ahead of them
-// the prefetch would delay this kernel's mainloop).
+// L2 prefetch job for the NEXT kernel's inputs: up to 4 contiguous regions (a weight's first row
+// blocks, or activation-stash blocks the next fused epilogue reads), split evenly over this grid's
+// CTAs, one bulk prefetch per CTA and region, issued by the producer thread after its own loads
+// (the TMA unit is a FIFO: queued ahead of them the prefetches would delay this kernel's mainloop).
 struct PrefetchJob {
-  const uint8_t* base;
-  long bytes;
+  const uint8_t* base[4];
+  long bytes[4];
 };
 __device__ __forceinline__ void l2_prefetch(const PrefetchJob& pj) {
-  if (pj.bytes <= 0) return;
   const long G = (long)gridDim.x * gridDim.y * gridDim.z;
   const long lin = blockIdx.x + (long)gridDim.x * (blockIdx.y + (long)gridDim.y * blockIdx.z);
-  const long chunk = ((pj.bytes + G - 1) / G + 15) / 16 * 16;
-  const long off = lin * chunk;
-  if (off >= pj.bytes) return;
-  const long n = min(chunk, pj.bytes - off);
-  ptx::bulk_prefetch_l2(pj.base + off, (uint32_t)n, ptx::policy_evict_last());
+  const uint64_t pol = ptx::policy_evict_last();
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    if (pj.bytes[r] <= 0) continue;
+    const long chunk = ((pj.bytes[r] + G - 1) / G + 15) / 16 * 16;
+    const long off = lin * chunk;
+    if (off >= pj.bytes[r]) continue;
+    ptx::bulk_prefetch_l2(pj.base[r] + off, (uint32_t)min(chunk, pj.bytes[r] - off), pol);
+  }
 }
 
 // Epilogue warps' common start: wait for the accumulator, then for the preceding grid (inputs
@@ -229,10 +240,10 @@ __device__ __forceinline__ void epi_begin(uint64_t* accf, bool have, uint64_t* t
 }
 
 #define MLSTM_TRACE_BEGIN()                                  \
-  __shared__ uint64_t tr_ts[6];                              \
+  __shared__ uint64_t tr_ts[10];                             \
   const bool tracing = g_trace != nullptr;                   \
   if (tracing && threadIdx.x == 0) {                         \
-    for (int k = 1; k < 6; ++k) tr_ts[k] = 0;                \
+    for (int k = 1; k < 10; ++k) tr_ts[k] = 0;               \
     tr_ts[0] = ptx::globaltimer();                           \
   }
 #define MLSTM_TRACE_SLOT(i) (tracing ? &tr_ts[i] : nullptr)
@@ -377,6 +388,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int kb0 = z * kb_per_split;
   const int nkb = max(0, min(kb_per_split, total_kb - kb0));
   float* part = scratch + ((long)(blockIdx.y * (gridDim.x / S) + tile_n) * S) * (128L * BN);
+  float* stageT = reinterpret_cast<float*>(L.sA);  // tile-epilogue staging: the stages are idle by then
   gemm_setup<C, false>(L, &tmA, &tmB, BN);
   ptx::tc_fence_before();
   __syncthreads();
@@ -432,8 +444,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
         const int col0 = n0 + cl;
-        if (row < M && col0 < N) epi.template run<NG>(row, col0, v);
+        if constexpr (HasTile<Epi>::value) {
+          float4* d = reinterpret_cast<float4*>(stageT + rl * (SLICE + 4) + (cl - z * SLICE));
+#pragma unroll
+          for (int i = 0; i < PIECE / 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        } else {
+          if (row < M && col0 < N) epi.template run<NG>(row, col0, v);
+        }
       }
+    }
+    if (tracing && threadIdx.x == 64) tr_ts[6] = ptx::globaltimer();
+    if constexpr (HasTile<Epi>::value) {
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (tracing && threadIdx.x == 64) tr_ts[7] = ptx::globaltimer();
+      const int c0 = n0 + z * SLICE;
+      if (m0 < M && c0 < N)
+        epi.tile(stageT, SLICE + 4, m0, c0, min(SLICE, N - c0), min(128, M - m0),
+                 reinterpret_cast<uint8_t*>(stageT + 128 * (SLICE + 4)), tid);
+      if (tracing && threadIdx.x == 64) tr_ts[8] = ptx::globaltimer();
     }
   }
   ptx::tc_fence_before();

@@ -497,6 +497,14 @@ __global__ void gather_x_kernel(Net<S> n, float* out) {
   }
 }
 
+// Deterministic pseudo-random fp16 fill in [-1, 1) (benchmark operands: realistic bit toggling).
+__global__ void random_half_kernel(__half* p, long count, uint64_t seed) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x) {
+    const double u = (double)(splitmix64_at(seed, (uint64_t)i) >> 11) * 0x1.0p-53;
+    p[i] = __float2half_rn((float)(2.0 * u - 1.0));
+  }
+}
+
 template <typename S>
 __global__ void to_float_kernel(const S* __restrict__ src, float* __restrict__ dst, long count) {
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x)

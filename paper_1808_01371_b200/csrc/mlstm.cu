@@ -88,6 +88,7 @@ struct mlstm_ctx {
   bool pdl = false;                   // programmatic dependent launch of the GEMMs (MLSTM_PDL=1; neutral)
   float pf_fwd = 0.f, pf_bwd = 0.f;   // L2 prefetch of the next W_h / W_h^T (MLSTM_PF_FWD/BWD; neutral,
                                       // profiles/r01_l2_prefetch.log)
+  bool pf_stash = true;               // backward: prefetch the next epilogue's stash blocks (MLSTM_PF_STASH)
   Net<__half> nh{};
   Net<float> nf{};
   ncclComm_t comm = nullptr;
@@ -284,6 +285,7 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   if (const char* v = getenv("MLSTM_PDL")) c->pdl = v[0] != '0';
   if (const char* v = getenv("MLSTM_PF_FWD")) c->pf_fwd = (float)atof(v);
   if (const char* v = getenv("MLSTM_PF_BWD")) c->pf_bwd = (float)atof(v);
+  if (const char* v = getenv("MLSTM_PF_STASH")) c->pf_stash = v[0] != '0';
   if (const char* v = getenv("MLSTM_L2_WH")) c->l2_wh = (float)atof(v);
   const char* dbg = getenv("MLSTM_DEBUG_SIMT_GEMM");  // test instrument: mixed mode on the SIMT engine
   c->tc = c->mixed && !(dbg && dbg[0] == '1');
@@ -405,7 +407,15 @@ cudaError_t launch_tc2(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* m
 // D[M x N] = A[az] . B[bz]^T, fused epilogue.  `splits` > 1 only with a partial epilogue.
 // Optional L2 prefetch of the next GEMM's weight operand (see l2_prefetch in gemm.cuh).
 struct Prefetch {
-  PrefetchJob job{nullptr, 0};
+  PrefetchJob job{{nullptr, nullptr, nullptr, nullptr}, {0, 0, 0, 0}};
+  int n = 0;
+  void add(const void* p, long bytes) {
+    if (n < 4 && bytes > 0) {
+      job.base[n] = static_cast<const uint8_t*>(p);
+      job.bytes[n] = bytes / 16 * 16;
+      ++n;
+    }
+  }
 };
 
 template <typename S, class Epi>
@@ -525,8 +535,7 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   const Plan p1 = plan_gemm(c->tc, B, h, h, false), p2 = plan_gemm(c->tc, B, 4 * h, h, false);
   // F1 (light on HBM) prefetches into L2 the first k-blocks of every W_h tile F2 will stream
   Prefetch pf1;
-  if (c->pf_fwd > 0 && c->tc)
-    pf1.job = PrefetchJob{reinterpret_cast<const uint8_t*>(n.Wh_w), (long)(c->pf_fwd * 8.0 * h * h) / 16 * 16};
+  if (c->pf_fwd > 0 && c->tc) pf1.add(n.Wh_w, (long)(c->pf_fwd * 8.0 * h * h));
   for (int t = 0; t < T; ++t) {
     RET_IF(gemm<S>(c, Hprev, t, Wmh, 0, B, h, h, p1, EpiF1<S>{n, t}, pf1));
     RET_IF(gemm<S>(c, Msc, 0, Wh, 0, B, 4 * h, h, p2, EpiF2<S>{n, t}));
@@ -569,12 +578,22 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
     const Opd WmhT{n.WmhT, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh), true};
     const Plan p1 = plan_gemm(c->tc, B, h, 4 * h, false), p2 = plan_gemm(c->tc, B, h, h, false);
     // B2 prefetches into L2 the first k-blocks (of each K split) of the W_h^T tiles B1 streams next
-    Prefetch pf2;
-    if (c->pf_bwd > 0 && c->tc)
-      pf2.job = PrefetchJob{reinterpret_cast<const uint8_t*>(n.WhT), (long)(c->pf_bwd * 8.0 * h * h) / 16 * 16};
+    const size_t es = sizeof(S);
     for (int t = T - 1; t >= 0; --t) {
-      RET_IF(gemm<S>(c, dZ, 0, WhT, 0, B, h, 4 * h, p1, EpiB1<S>{n, t}));
-      if (t > 0) RET_IF(gemm<S>(c, dA, 0, WmhT, 0, B, h, h, p2, EpiB2<S>{n, t - 1}, pf2));
+      // B1(t) prefetches what B2's gate backward of step t-1 reads (written long ago by the
+      // forward: gates, c_{t-1} and c_{t-2} (adjacent blocks), dH_dec); B2 prefetches the a-stash
+      // block the next B1 reads.
+      Prefetch pb1, pb2;
+      if (c->pf_stash && c->tc && t > 0) {
+        const long BH = (long)B * h;
+        pb1.add(n.Gates + (long)(t - 1) * 4 * BH, 4 * BH * (long)es);
+        pb1.add(n.Crm + (long)(t - 1) * BH, 2 * BH * 4L);
+        pb1.add(n.dHdec + (long)(t - 1) * BH, BH * 4L);
+        pb2.add(n.Astash + (long)(t - 1) * BH, BH * (long)es);
+      }
+      if (c->pf_bwd > 0 && c->tc) pb2.add(n.WhT, (long)(c->pf_bwd * 8.0 * h * h));
+      RET_IF(gemm<S>(c, dZ, 0, WhT, 0, B, h, 4 * h, p1, EpiB1<S>{n, t}, pb1));
+      if (t > 0) RET_IF(gemm<S>(c, dA, 0, WmhT, 0, B, h, h, p2, EpiB2<S>{n, t - 1}, pb2));
     }
   }
   phase(c, PH_WGRAD);
@@ -1181,8 +1200,9 @@ mlstm_status mlstm_gemm_bench(int engine, int M, int N, int K, int bn, int iters
     return fail(MLSTM_ECUDA, "cudaMalloc");
   }
   const long nA = (long)M * K, nB = (long)N * K;
-  cudaMemset(A, 0x3c, 2L * M * K);  // operand values do not matter for timing
-  cudaMemset(B, 0x3c, 2L * N * K);
+  // random operands: constant bit patterns draw less tensor-core power and overstate throughput
+  random_half_kernel<<<grid_for(nA), 256>>>(A, nA, 1);
+  random_half_kernel<<<grid_for(nB), 256>>>(B, nB, 2);
   Opd oa{A, M, K, K, 1, nA}, ob{B, N, K, K, 1, nB, 0, true};
   Plan p = plan_gemm(true, M, N, K, false);
   if (engine != 3) {

@@ -142,6 +142,33 @@ __device__ __forceinline__ void ld16(const float* src, float* v) {
   }
 }
 
+// 4 consecutive values (8-byte fp16 / 16-byte fp32 vectors; callers keep them aligned).
+__device__ __forceinline__ float4 ld4(const __half* p) {
+  const uint2 w = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(__half* p, float4 v) {
+  uint2 w;
+  *reinterpret_cast<__half2*>(&w.x) = __floats2half2_rn(v.x, v.y);
+  *reinterpret_cast<__half2*>(&w.y) = __floats2half2_rn(v.z, v.w);
+  *reinterpret_cast<uint2*>(p) = w;
+}
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+// 4 values to shared memory at a 2-element-aligned address (fp16: two 4-byte stores).
+__device__ __forceinline__ void st4s(__half* p, float4 v) {
+  reinterpret_cast<__half2*>(p)[0] = __floats2half2_rn(v.x, v.y);
+  reinterpret_cast<__half2*>(p)[1] = __floats2half2_rn(v.z, v.w);
+}
+__device__ __forceinline__ void st4s(float* p, float4 v) {
+  p[0] = v.x;
+  p[1] = v.y;
+  p[2] = v.z;
+  p[3] = v.w;
+}
+
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-x)); }
 
 // Gate nonlinearities.  Mixed mode (S = __half): the hardware tanh.approx.f32 (MUFU, max relative

@@ -215,7 +215,7 @@ def mlstm_trace_enable(capacity: int) -> None:
 
 
 def mlstm_trace_read(capacity: int = 1 << 20) -> np.ndarray:
-    out = np.zeros((capacity, 8), dtype=np.uint64)
+    out = np.zeros((capacity, 12), dtype=np.uint64)
     n = ctypes.c_int32()
     _check(lib().mlstm_trace_read(out.ctypes.data_as(_P(ctypes.c_uint64)), capacity, ctypes.byref(n)))
     return out[: n.value]

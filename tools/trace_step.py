@@ -36,8 +36,21 @@ for L in launches:
                             d(6, 7) if (R[:, 6] > 0).any() else d(5, 7), (st - prev_end) if prev_end else np.nan,
                             len(R)])
     prev_end = en
+R6 = rec[(rec[:, 8] > 0)]
+if len(R6):
+    for tag in sorted(set(R6[:, 0].tolist())):
+        X = R6[R6[:, 0] == tag]
+        print(f"  {names.get(tag, tag)} split-K epilogue: reduce {np.mean(X[:, 8] - X[:, 6]) / 1e3:.2f} us, "
+              f"tile {np.mean(np.where(X[:, 10] > 0, X[:, 10] - X[:, 9], 0)) / 1e3:.2f} us, "
+              f"after {np.mean(X[:, 7] - np.maximum(X[:, 8], X[:, 10])) / 1e3:.2f} us")
 print("tag      n   span_us  start->tma  tma->data  data->acc  acc->reduced  ->end  gap_before  ctas")
 for tag, v in sorted(stats.items()):
     a = np.nanmean(np.array(v, dtype=float), axis=0) / 1e3
     print(f"{names.get(tag, tag):8s} {len(v):4d} {a[0]:8.2f} {a[1]:10.2f} {a[2]:10.2f} {a[3]:10.2f} {a[4]:12.2f} "
           f"{a[5]:7.2f} {a[6]:10.2f} {a[7]*1e3:6.0f}")
+print("\nper-launch (wgrad / dec / dHdec / tab):")
+for L in launches:
+    if L["tag"] in (5, 6, 7, 8):
+        R = np.array(L["rows"])
+        print(f"  {names.get(L['tag'])}: span {(R[:, 7].max() - R[:, 2].min()) / 1e3:9.1f} us, ctas {len(R)}, "
+              f"mean cta {(R[:, 7] - R[:, 2]).mean() / 1e3:8.1f} us")
