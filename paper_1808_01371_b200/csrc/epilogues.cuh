@@ -20,6 +20,14 @@ struct EpiTab {
     float* dst = n.tab + (long)row * 5 * n.h + col0;
 #pragma unroll
     for (int q = 0; q < NG; ++q) st16(dst + 16 * q, v + 16 * q);
+    if (n.XZT && col0 >= n.h) {  // transposed fp16 (W_x E + b) for the folded F2 (lanes = bytes)
+      const float* bias = n.master + n.po.b;
+#pragma unroll
+      for (int i = 0; i < 16 * NG; ++i) {
+        const int r = col0 - n.h + i;
+        n.XZT[(long)r * 256 + row] = to_s<S>(v[i] + bias[canon_of_int(r, n.h)]);
+      }
+    }
   }
 };
 
@@ -52,32 +60,39 @@ struct EpiF1 {
   }
 };
 
-// (b) forward GEMM 2, Z_t = M_t W_h^T (+ W_x x_t + b): gates, cell update, hidden state.
+// (b) forward GEMM 2, Z_t = M_t W_h^T (+ W_x x_t + b): gates, cell update, hidden state.  With
+// `folded` the GEMM's second K segment (one-hot x (W_x E + b)^T) already added W_x x_t + b.
 template <typename S>
 struct EpiF2 {  // one call = 4 gates x 16 units: NG must be 4
   static constexpr int kMinGroups = 4;  // 16-column groups one call must cover
   __device__ __forceinline__ void operator()(int row, int col0, float (&v)[64]) const { run<4>(row, col0, v); }
   Net<S> n;
   int t;
+  int folded;
   template <int NG>
   __device__ __forceinline__ void run(int b, int col0, const float* v) const {
     const int h = n.h;
     const int j0 = (col0 >> 6) * 16;
-    const float* xz = n.tab + (long)n.byte_at(b, t) * 5 * h + h + col0;
     const float* bias = n.master + n.po.b;
     float xv[64];
+    if (folded) {
 #pragma unroll
-    for (int q = 0; q < NG; ++q) ld16(xz + 16 * q, xv + 16 * q);
+      for (int i = 0; i < 64; ++i) xv[i] = 0.f;
+    } else {
+      const float* xz = n.tab + (long)n.byte_at(b, t) * 5 * h + h + col0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ld16(xz + 16 * q, xv + 16 * q);
+    }
     float cprev[16];
     ld16(n.Crm + ((long)t * n.B + b) * h + j0, cprev);
     float gi[16], gf[16], go[16], gu[16], cv[16], hv[16];
 #pragma unroll
     for (int jj = 0; jj < 16; ++jj) {
       const int j = j0 + jj;
-      const float zi = v[jj] + xv[jj] + bias[j];
-      const float zf = v[16 + jj] + xv[16 + jj] + bias[h + j];
-      const float zo = v[32 + jj] + xv[32 + jj] + bias[2 * h + j];
-      const float zu = v[48 + jj] + xv[48 + jj] + bias[3 * h + j];
+      const float zi = v[jj] + (folded ? 0.f : xv[jj] + bias[j]);
+      const float zf = v[16 + jj] + (folded ? 0.f : xv[16 + jj] + bias[h + j]);
+      const float zo = v[32 + jj] + (folded ? 0.f : xv[32 + jj] + bias[2 * h + j]);
+      const float zu = v[48 + jj] + (folded ? 0.f : xv[48 + jj] + bias[3 * h + j]);
       gi[jj] = act_sigmoid<S>(zi);
       gf[jj] = act_sigmoid<S>(zf);
       go[jj] = act_sigmoid<S>(zo);

@@ -129,20 +129,34 @@ __device__ __forceinline__ void gemm_setup(const SmemLayout<C>& L, const CUtenso
 // peer's bytes may land first (transiently negative tx-count); the peer cannot run a phase ahead
 // because it waits on its own empty barrier, released by the same multicast commit.  (A
 // release.cluster remote arrive here would fence every prior TMA and serialise the pipeline.)
+// K runs over two segments: k-blocks [0, kb_seg0) from (A, B), then from (A2, B2) -- used to fold
+// a one-hot x table product (input projection + bias) into the recurrent GEMM's accumulator.
+struct Seg2 {
+  int kb_seg0;  // k-blocks of the first segment
+  int az2, bz2;
+};
+
 template <class C, bool PAIR>
 __device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUtensorMap* tmA, const CUtensorMap* tmB,
-                                             int nkb, int kb0, int m0, int nb0, int az, int bz, uint32_t polA,
+                                             const CUtensorMap* tmA2, const CUtensorMap* tmB2, Seg2 sg, int nkb,
+                                             int kb0, int m0, int nb0, int az, int bz, uint32_t polA,
                                              uint32_t polB, int flags, bool leader, uint32_t bar_leader0,
                                              uint64_t* trace_slot) {
   const uint64_t pa = ptx::make_policy(polA), pb = ptx::make_policy(polB);
   const uint32_t tx = PAIR ? 2 * C::STAGE_BYTES : C::STAGE_BYTES;
   auto loadA = [&](int s, int kb) {
-    if (PAIR) ptx::tma_load_3d_2sm(L.sA + s * C::A_BYTES, tmA, bar_leader0 + s * 8, kb * C::BK, m0, az, pa);
-    else ptx::tma_load_3d(L.sA + s * C::A_BYTES, tmA, &L.full[s], kb * C::BK, m0, az, pa);
+    const bool s2 = kb >= sg.kb_seg0;
+    const CUtensorMap* m = s2 ? tmA2 : tmA;
+    const int k = (s2 ? kb - sg.kb_seg0 : kb) * C::BK, z = s2 ? sg.az2 : az;
+    if (PAIR) ptx::tma_load_3d_2sm(L.sA + s * C::A_BYTES, m, bar_leader0 + s * 8, k, m0, z, pa);
+    else ptx::tma_load_3d(L.sA + s * C::A_BYTES, m, &L.full[s], k, m0, z, pa);
   };
   auto loadB = [&](int s, int kb) {
-    if (PAIR) ptx::tma_load_3d_2sm(L.sB + s * C::B_BYTES, tmB, bar_leader0 + s * 8, kb * C::BK, nb0, bz, pb);
-    else ptx::tma_load_3d(L.sB + s * C::B_BYTES, tmB, &L.full[s], kb * C::BK, nb0, bz, pb);
+    const bool s2 = kb >= sg.kb_seg0;
+    const CUtensorMap* m = s2 ? tmB2 : tmB;
+    const int k = (s2 ? kb - sg.kb_seg0 : kb) * C::BK, z = s2 ? sg.bz2 : bz;
+    if (PAIR) ptx::tma_load_3d_2sm(L.sB + s * C::B_BYTES, m, bar_leader0 + s * 8, k, nb0, z, pb);
+    else ptx::tma_load_3d(L.sB + s * C::B_BYTES, m, &L.full[s], k, nb0, z, pb);
   };
   const int pre = (flags & kGemmStaticB) ? min(C::STAGES, nkb) : 0;
   for (int i = 0; i < pre; ++i) {
@@ -256,7 +270,8 @@ __device__ __forceinline__ void epi_begin(uint64_t* accf, bool have, uint64_t* t
 // ---------------------------------------------------------------------------------------------
 template <int BN, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, Seg2 sg, int M,
                    int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, int flags,
                    PrefetchJob pj, Epi epi) {
   using C = TcCfg<BN>;
@@ -276,7 +291,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       if (nkb > 0)
-        gemm_produce<C, false>(L, &tmA, &tmB, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true, 0,
+        gemm_produce<C, false>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true, 0,
                                MLSTM_TRACE_SLOT(1));
       l2_prefetch(pj);
     }
@@ -306,7 +321,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // ---------------------------------------------------------------------------------------------
 template <int BN, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
-    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, Seg2 sg, int M,
                     int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, int flags,
                     PrefetchJob pj, Epi epi) {
   using C = Tc2Cfg<BN>;
@@ -329,7 +345,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       if (nkb > 0)
-        gemm_produce<C, true>(L, &tmA, &tmB, nkb, kb0, m0, n0 + rank * (BN / 2), az, bz, polA, polB, flags,
+        gemm_produce<C, true>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0 + rank * (BN / 2), az, bz, polA, polB, flags,
                               leader, ptx::mapa_shared(ptx::smem_u32(&L.full[0]), 0), MLSTM_TRACE_SLOT(1));
       l2_prefetch(pj);
     }
@@ -365,7 +381,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 // half a row of the slice, or a whole row when the epilogue needs full 64-column chunks.
 template <int S, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    gemm_tc1s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+    gemm_tc1s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, Seg2 sg, int M,
                      int N, int K, int az, int bz, int kb_per_split, uint32_t polA, uint32_t polB, int flags,
                      PrefetchJob pj, float* __restrict__ scratch,
                      Epi epi) {
@@ -397,7 +414,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       if (nkb > 0)
-        gemm_produce<C, false>(L, &tmA, &tmB, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true, 0,
+        gemm_produce<C, false>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true, 0,
                                MLSTM_TRACE_SLOT(1));
       l2_prefetch(pj);
     }

@@ -118,6 +118,12 @@ __global__ void onehot_kernel(Net<S> n) {
     const int v0 = n.byte_at(b, t);
     const long kc = n.kcol(t, b);
     for (int v = 0; v < 256; ++v) n.OHT[(long)v * n.ldK + kc] = to_s<S>(v == v0 ? 1.f : 0.f);
+    if (n.OHR) {
+      S* row = n.OHR + i * 256;
+      for (int v = 0; v < 256; v += 4)
+        st4(row + v, make_float4(v == v0 ? 1.f : 0.f, v + 1 == v0 ? 1.f : 0.f, v + 2 == v0 ? 1.f : 0.f,
+                                 v + 3 == v0 ? 1.f : 0.f));
+    }
   }
 }
 

@@ -208,6 +208,8 @@ void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
   n.bytes = c->bytes;
   n.reset = c->reset;
   n.tab = cv.take<float>(256L * 5 * h);
+  n.XZT = c->tc ? cv.take<S>(4L * h * 256) : nullptr;
+  n.OHR = c->tc ? cv.take<S>((long)T * B * 256) : nullptr;
   n.Hrm = cv.take<S>((long)(T + 1) * B * h);
   n.HT = cv.take<S>((long)h * c->ldH);
   n.Crm = cv.take<float>((long)(T + 1) * B * h);
@@ -378,30 +380,33 @@ cudaError_t launch_gemm(mlstm_ctx* c, Kern kern, dim3 grid, int smem, int cluste
 }
 
 template <int BN, class Epi>
-cudaError_t launch_tc(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az, int bz,
+cudaError_t launch_tc(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, const CUtensorMap* ma2,
+                      const CUtensorMap* mb2, Seg2 sg, int M, int N, int K, int az, int bz,
                       uint32_t pa, uint32_t pb, int flags, int splits, PrefetchJob pj,
                       const Epi& epi) {
   const int kb = (K + 63) / 64, kbps = (kb + splits - 1) / splits;
   return launch_gemm(c, gemm_tc_kernel<BN, Epi>, dim3((N + BN - 1) / BN, (M + 127) / 128, splits), TcCfg<BN>::SMEM,
-                     1, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, flags, pj, epi);
+                     1, *ma, *mb, *ma2, *mb2, sg, M, N, K, az, bz, kbps, pa, pb, flags, pj, epi);
 }
 
 template <int S, class Epi>
-cudaError_t launch_tc1s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az,
+cudaError_t launch_tc1s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, const CUtensorMap* ma2,
+                        const CUtensorMap* mb2, Seg2 sg, int M, int N, int K, int az,
                         int bz, uint32_t pa, uint32_t pb, int flags, PrefetchJob pj,
                         const Epi& epi) {
   const int kb = (K + 63) / 64, kbps = (kb + S - 1) / S;
   return launch_gemm(c, gemm_tc1s_kernel<S, Epi>, dim3(S * ((N + 255) / 256), (M + 127) / 128, 1), TcCfg<256>::SMEM,
-                     S, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, flags, pj, c->split_scratch, epi);
+                     S, *ma, *mb, *ma2, *mb2, sg, M, N, K, az, bz, kbps, pa, pb, flags, pj, c->split_scratch, epi);
 }
 
 template <int BN, class Epi>
-cudaError_t launch_tc2(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, int M, int N, int K, int az,
+cudaError_t launch_tc2(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, const CUtensorMap* ma2,
+                       const CUtensorMap* mb2, Seg2 sg, int M, int N, int K, int az,
                        int bz, uint32_t pa, uint32_t pb, int flags, int splits, PrefetchJob pj,
                        const Epi& epi) {
   const int kb = (K + 63) / 64, kbps = (kb + splits - 1) / splits;
   return launch_gemm(c, gemm_tc2_kernel<BN, Epi>, dim3(2 * ((N + BN - 1) / BN), (M + 255) / 256, splits),
-                     Tc2Cfg<BN>::SMEM, 2, *ma, *mb, M, N, K, az, bz, kbps, pa, pb, flags, pj, epi);
+                     Tc2Cfg<BN>::SMEM, 2, *ma, *mb, *ma2, *mb2, sg, M, N, K, az, bz, kbps, pa, pb, flags, pj, epi);
 }
 
 // D[M x N] = A[az] . B[bz]^T, fused epilogue.  `splits` > 1 only with a partial epilogue.
@@ -418,9 +423,17 @@ struct Prefetch {
   }
 };
 
+// Optional second K segment (A2[az2] . B2^T added into the same accumulator; tcgen05 engines only).
+struct Segment {
+  const Opd* A2 = nullptr;
+  int az2 = 0;
+  const Opd* B2 = nullptr;
+  int K2 = 0;
+};
+
 template <typename S, class Epi>
 mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int M, int N, int K, Plan p,
-                  const Epi& epi, const Prefetch& pf = Prefetch{}) {
+                  const Epi& epi, const Prefetch& pf = Prefetch{}, const Segment& seg = Segment{}) {
   if constexpr (std::is_same<S, __half>::value) {
     if (c->tc) {
     const CUtensorMap* ma = get_map(c, A, 128);
@@ -432,20 +445,28 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
     cudaError_t e;
     const int gflags = B.weight ? kGemmStaticB : 0;
     const PrefetchJob pj = pf.job;
+    const CUtensorMap* ma2 = seg.A2 ? get_map(c, *seg.A2, 128) : ma;
+    const CUtensorMap* mb2 = seg.B2 ? get_map(c, *seg.B2, p.pair ? p.bn / 2 : p.bn) : mb;
+    if (!ma2 || !mb2) {
+      c->failed = MLSTM_ECUDA;
+      return MLSTM_ECUDA;
+    }
+    const Seg2 sg{seg.A2 ? (K + 63) / 64 : (1 << 30), seg.az2, 0};
+    const int Kt = seg.A2 ? ((K + 63) / 64) * 64 + seg.K2 : K;  // the kernels' K runs over both segments
     if (p.cluster) {
-      e = p.splits == 2 ? launch_tc1s<2>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, pj, epi)
-                        : launch_tc1s<4>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, pj, epi);
+      e = p.splits == 2 ? launch_tc1s<2>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi)
+                        : launch_tc1s<4>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi);
     } else if (p.pair) {
       switch (p.bn) {
-        case 256: e = launch_tc2<256>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
-        case 128: e = launch_tc2<128>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
-        default: e = launch_tc2<64>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
+        case 256: e = launch_tc2<256>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
+        case 128: e = launch_tc2<128>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
+        default: e = launch_tc2<64>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
       }
     } else {
       switch (p.bn) {
-        case 256: e = launch_tc<256>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
-        case 128: e = launch_tc<128>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
-        default: e = launch_tc<64>(c, ma, mb, M, N, K, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
+        case 256: e = launch_tc<256>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
+        case 128: e = launch_tc<128>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
+        default: e = launch_tc<64>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
       }
     }
     CUDA_OR_FAIL(c, e);
@@ -519,6 +540,7 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   const int h = c->h, e = c->e, B = c->B, T = c->T;
   phase(c, PH_PREP);
   LAUNCH(c, (state_in_kernel<S><<<grid_for((long)B * h), 256, 0, c->stream>>>(n, slot)));
+  if (n.OHR) LAUNCH(c, (onehot_kernel<S><<<grid_for((long)T * B), 256, 0, c->stream>>>(n)));
   phase(c, PH_TAB);
   {
     Opd A{n.E_w, 256, e, e, 1, 256L * e};
@@ -532,13 +554,24 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   const Opd Wmh{n.Wmh_w, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh), true};
   const Opd Msc{n.Mscr, B, h, h, 1, (long)B * h, kPolFirst};
   const Opd Wh{n.Wh_w, 4L * h, h, h, 1, 4L * h * h, pol_last(c->l2_wh), true};
-  const Plan p1 = plan_gemm(c->tc, B, h, h, false), p2 = plan_gemm(c->tc, B, 4 * h, h, false);
+  const Plan p1 = plan_gemm(c->tc, B, h, h, false), p2 = plan_gemm(c->tc, B, 4 * h, h + 256, false);
+  // tcgen05 path: W_x x_t + b enters F2's accumulator as a second K segment, one-hot(bytes_t) x
+  // (W_x E + b)^T (exact selection of one table row; the table is rounded to fp16)
+  const Opd OH{n.OHR, B, 256, 256, T, (long)B * 256, kPolFirst};
+  const Opd XZ{n.XZT, 4L * h, 256, 256, 1, 4L * h * 256, 0, true};
+  Segment seg2;
+  if (n.OHR) {
+    seg2.A2 = &OH;
+    seg2.B2 = &XZ;
+    seg2.K2 = 256;
+  }
   // F1 (light on HBM) prefetches into L2 the first k-blocks of every W_h tile F2 will stream
   Prefetch pf1;
   if (c->pf_fwd > 0 && c->tc) pf1.add(n.Wh_w, (long)(c->pf_fwd * 8.0 * h * h));
   for (int t = 0; t < T; ++t) {
     RET_IF(gemm<S>(c, Hprev, t, Wmh, 0, B, h, h, p1, EpiF1<S>{n, t}, pf1));
-    RET_IF(gemm<S>(c, Msc, 0, Wh, 0, B, 4 * h, h, p2, EpiF2<S>{n, t}));
+    seg2.az2 = t;
+    RET_IF(gemm<S>(c, Msc, 0, Wh, 0, B, 4 * h, h, p2, EpiF2<S>{n, t, n.OHR != nullptr}, Prefetch{}, seg2));
   }
   phase(c, PH_DEC);
   {
@@ -557,7 +590,7 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
   RET_IF(enqueue_forward<S>(c, MLSTM_SLOT_TRAIN));
   // the one-hot and the dC reset belong to the prep phase logically; they run here, off the
   // forward's critical path
-  LAUNCH(c, (onehot_kernel<S><<<grid_for((long)T * B), 256, 0, c->stream>>>(n)));
+  if (!n.OHR) LAUNCH(c, (onehot_kernel<S><<<grid_for((long)T * B), 256, 0, c->stream>>>(n)));
   CUDA_OR_FAIL(c, cudaMemsetAsync(n.dC, 0, sizeof(float) * (size_t)B * h, c->stream));
   phase(c, PH_CE);
   const double denom = (double)B * c->world * T;  // B_g * T (Q7)

@@ -63,6 +63,8 @@ struct Net {
   S *E_w, *Wcat_w, *Wmh_w, *Wh_w, *Wdec_w, *WmhT, *WhT, *WdecT;
   // activations / stash
   float* tab;     // [256][5h]: cols [0,h) = W_mx E^T (mx table), [h,5h) = W_x E^T in internal order
+  S* XZT;         // [4h][256] (W_x E^T + b)^T in internal row order: F2's second K segment (mixed mode)
+  S* OHR;         // [T][B][256] one-hot of the input bytes, row-major: F2's second A segment
   S* Hrm;         // [(T+1)][B][h]; block 0 = h0, block t+1 = H_t
   S* HT;          // [h][ldH]; column t*Bp+b = Hrm[t][b]
   float* Crm;     // [(T+1)][B][h]
