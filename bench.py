@@ -37,8 +37,11 @@ CONFIGS = {
     "C2": (1024, 64, 128, 64, "mLSTM h=1024 e=64, seq 64, batch 128/GPU"),
     "C3": (4096, 64, 256, 256, "paper model: mLSTM h=4096 e=64, seq 256, batch 256/GPU, fp16/fp32 mixed, "
                                "dynamic loss scaling"),
+    "C4": (4096, 64, 4096, 256, "large batch: mLSTM h=4096 e=64, seq 256, 4096 rows/GPU as 4 x 1024-row "
+                                "micro-batches (global batch 32768 at 8 GPUs), fp16/fp32 mixed"),
     "C5": (8192, 64, 128, 256, "8192-d mLSTM e=64, seq 256, batch 128/GPU, fp16/fp32 mixed"),
 }
+MICRO_BATCH = {"C4": 1024}
 DEVSTATE_BYTES = 56  # the device scalar block the step copies back (loss, alpha, lr, skip, it, tau)
 
 
@@ -210,7 +213,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     h, e, B, T, desc = CONFIGS[args.config]
-    cfg = M.mlstm_default_config(hidden=h, embed=e, batch=B, seq_len=T, precision=M.MLSTM_MIXED)
+    cfg = M.mlstm_default_config(hidden=h, embed=e, batch=B, seq_len=T, precision=M.MLSTM_MIXED,
+                                 micro_batch=MICRO_BATCH.get(args.config, 0))
     nid = None
     if world > 1:
         t = torch.zeros(128, dtype=torch.uint8, device="cuda")

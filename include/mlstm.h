@@ -53,7 +53,9 @@ typedef struct {
   int32_t vocab;        /* must be 256: byte level                                */
   int32_t seq_len;      /* T: TBTT window, 256                                         */
   int32_t batch;        /* B: rows per rank ("local batch"); global batch = B * world   */
-  int32_t micro_batch;  /* reserved, must be 0 (= batch) in this version                       */
+  int32_t micro_batch;  /* rows per micro-batch (0 = batch); must divide batch.  Each step runs the
+                           forward/backward per micro-batch and accumulates gradients in fp32
+                           (P:130), then one allreduce + one update (4096 rows/GPU)    */
   int32_t precision;    /* MLSTM_MIXED (fp16 storage/multiply, fp32 accumulate) or MLSTM_FP32   */
   int32_t weight_norm;  /* reserved, must be 0 (Q4)                                            */
   uint64_t seed;        /* parameter init: counter-based SplitMix64, U(+-1/sqrt(cols)) (Q12)   */
@@ -122,7 +124,7 @@ mlstm_status mlstm_train_step(mlstm_ctx* ctx, const uint8_t* bytes, const uint8_
 mlstm_status mlstm_train_step_host(mlstm_ctx* ctx, const uint8_t* bytes_host,
                                    const uint8_t* reset_host, mlstm_step_result* out);
 
-/* Forward-only evaluation of one window of Be <= B rows from the eval-slot state (state
+/* Forward-only evaluation of one window of Be <= micro-batch rows from the eval-slot state (state
  * persisted across evaluation minibatches; no update).  bytes: device uint8 [Be][T+1].
  * Outputs (host): nats_sum = global sum of per-position CE (all ranks), tokens = Be*T*world,
  * bpc = nats_sum/tokens*log2(e). */
@@ -141,7 +143,7 @@ mlstm_status mlstm_set_params(mlstm_ctx* ctx, const float* host_in);  /* also re
  * canonical layout, fp32 (read back from the reduced fp16 (mixed) / fp32 buffer). */
 mlstm_status mlstm_get_grads(mlstm_ctx* ctx, float* host_out);
 
-/* Persisted state of a slot (MLSTM_SLOT_TRAIN / MLSTM_SLOT_EVAL): h and c, fp32 [B][h] each. */
+/* Persisted state of a slot (MLSTM_SLOT_TRAIN / MLSTM_SLOT_EVAL): h and c, fp32 [batch][h] each. */
 mlstm_status mlstm_get_state(mlstm_ctx* ctx, int slot, float* h_out, float* c_out);
 mlstm_status mlstm_set_state(mlstm_ctx* ctx, int slot, const float* h_in, const float* c_in);
 

@@ -88,12 +88,14 @@ __global__ void transpose_kernel(const S* __restrict__ src, S* __restrict__ dst,
 template <typename S>
 __global__ void state_in_kernel(Net<S> n, int slot) {
   const long BH = (long)n.B * n.h;
+  // this micro-batch's rows of the persisted state
+  const long so = (long)slot * n.Bfull * n.h + (long)n.st->mb * BH;
   if (blockIdx.x == 0 && threadIdx.x == 0) n.st->overflow = 0;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < BH; i += (long)gridDim.x * blockDim.x) {
     const int b = (int)(i / n.h), j = (int)(i % n.h);
     const bool rst = n.reset[b] != 0;
-    const S hv = rst ? to_s<S>(0.f) : n.hstate[slot * BH + i];
-    const float cv = rst ? 0.f : n.cstate[slot * BH + i];
+    const S hv = rst ? to_s<S>(0.f) : n.hstate[so + i];
+    const float cv = rst ? 0.f : n.cstate[so + i];
     n.Hrm[i] = hv;
     n.HT[(long)j * n.ldH + b] = hv;
     n.Crm[i] = cv;
@@ -103,9 +105,27 @@ __global__ void state_in_kernel(Net<S> n, int slot) {
 template <typename S>
 __global__ void state_out_kernel(Net<S> n, int slot) {
   const long BH = (long)n.B * n.h;
+  const long so = (long)slot * n.Bfull * n.h + (long)n.st->mb * BH;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < BH; i += (long)gridDim.x * blockDim.x) {
-    n.hstate[slot * BH + i] = n.Hrm[(long)n.T * BH + i];
-    n.cstate[slot * BH + i] = n.Crm[(long)n.T * BH + i];
+    n.hstate[so + i] = n.Hrm[(long)n.T * BH + i];
+    n.cstate[so + i] = n.Crm[(long)n.T * BH + i];
+  }
+}
+
+// Sets the micro-batch index the following kernels work on.
+__global__ void set_microbatch_kernel(DevState* st, int mb) { st->mb = mb; }
+
+// Micro-batch gradient accumulation in fp32 (the paper accumulates into fp32 masters):
+// gacc = (mb == 0 ? 0 : gacc) + g; after the last micro-batch the sum goes back to the fp16 arena
+// (the allreduce payload; an fp16 overflow of the sum is caught by the overflow check).
+template <typename S>
+__global__ void grad_accum_kernel(Net<S> n) {
+  const int mb = n.st->mb;
+  const bool first = mb == 0, last = mb == n.nmb - 1;
+  for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n.po.P; q += (long)gridDim.x * blockDim.x) {
+    const float g = (first ? 0.f : n.gacc[q]) + to_f(n.arena[q]);
+    if (last) n.arena[q] = to_s<S>(g);
+    else n.gacc[q] = g;
   }
 }
 
@@ -239,7 +259,7 @@ __global__ void __launch_bounds__(256) ce_reduce_kernel(Net<S> n, int nblk, int 
     if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) n.st->loss_sum = red[0];
+  if (threadIdx.x == 0) n.st->loss_sum = (n.st->mb == 0 ? 0.0 : n.st->loss_sum) + red[0];
   if (with_grad) {
     const int v = threadIdx.x;
     float cs = 0.f;

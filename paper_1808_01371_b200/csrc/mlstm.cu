@@ -69,7 +69,8 @@ struct mlstm_ctx {
   cudaStream_t cap = nullptr;      // private stream graphs are recorded on (the caller's may be
                                    // the legacy default stream, which cannot be captured)
   bool mixed = true, tc = true;
-  int h = 0, e = 0, B = 0, T = 0, Bp = 0;
+  int h = 0, e = 0, B = 0, T = 0, Bp = 0;  // B = rows per micro-batch
+  int Bfull = 0, nmb = 1;                    // rows per rank, micro-batches per step
   long ldK = 0, ldH = 0, P = 0, Kt = 0;
   ParamOffsets po{};
   uint8_t* ws = nullptr;
@@ -190,6 +191,7 @@ void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
   const int h = c->h, e = c->e, B = c->B, T = c->T;
   const long P = c->P;
   n.h = h; n.e = e; n.B = B; n.T = T; n.Bp = c->Bp;
+  n.Bfull = c->Bfull; n.nmb = c->nmb;
   n.ldK = c->ldK; n.ldH = c->ldH; n.po = c->po;
   n.master = cv.take<float>(P);
   c->adam_m = cv.take<float>(P);
@@ -243,8 +245,9 @@ void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
   n.part = cv.take<float>(part);
   c->split_scratch = c->tc ? cv.take<float>(kSplitScratchFloats) : nullptr;
   n.Scan = cv.take<float>(256L * 5 * h);
-  n.hstate = cv.take<S>(2L * B * h);
-  n.cstate = cv.take<float>(2L * B * h);
+  n.hstate = cv.take<S>(2L * c->Bfull * h);
+  n.cstate = cv.take<float>(2L * c->Bfull * h);
+  n.gacc = c->nmb > 1 ? cv.take<float>(P) : nullptr;
   c->nblk_ce = (int)(((long)T * B + 31) / 32);
   n.loss_part = cv.take<double>(c->nblk_ce);
   n.colsum_part = cv.take<float>((long)c->nblk_ce * 256);
@@ -259,8 +262,8 @@ mlstm_status validate(const mlstm_config* cfg) {
   if (cfg->embed <= 0 || cfg->embed % 64) return fail(MLSTM_EINVAL, "embed must be a positive multiple of 64");
   if (cfg->vocab != 256) return fail(MLSTM_EINVAL, "vocab must be 256 (byte level)");
   if (cfg->seq_len <= 0 || cfg->batch <= 0) return fail(MLSTM_EINVAL, "seq_len and batch must be positive");
-  if (cfg->micro_batch != 0 && cfg->micro_batch != cfg->batch)
-    return fail(MLSTM_EINVAL, "micro_batch must be 0 in this version");
+  if (cfg->micro_batch < 0 || (cfg->micro_batch > 0 && cfg->batch % cfg->micro_batch != 0))
+    return fail(MLSTM_EINVAL, "micro_batch must be 0 (= batch) or divide batch");
   if (cfg->weight_norm != 0) return fail(MLSTM_EINVAL, "weight_norm must be 0 in this version (DESIGN Q4)");
   if (cfg->precision != MLSTM_FP32 && cfg->precision != MLSTM_MIXED) return fail(MLSTM_EINVAL, "bad precision");
   if (!(cfg->decay_iters > 0) || !(cfg->lr0 >= 0)) return fail(MLSTM_EINVAL, "bad LR schedule");
@@ -274,7 +277,9 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   c->cfg = *cfg;
   c->h = cfg->hidden;
   c->e = cfg->embed;
-  c->B = cfg->batch;
+  c->Bfull = cfg->batch;
+  c->B = cfg->micro_batch > 0 ? cfg->micro_batch : cfg->batch;  // rows per micro-batch
+  c->nmb = c->Bfull / c->B;
   c->T = cfg->seq_len;
   c->Bp = (int)rup(c->B, 8);
   c->Kt = (long)c->T * c->Bp;
@@ -593,7 +598,7 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
   if (!n.OHR) LAUNCH(c, (onehot_kernel<S><<<grid_for((long)T * B), 256, 0, c->stream>>>(n)));
   CUDA_OR_FAIL(c, cudaMemsetAsync(n.dC, 0, sizeof(float) * (size_t)B * h, c->stream));
   phase(c, PH_CE);
-  const double denom = (double)B * c->world * T;  // B_g * T (Q7)
+  const double denom = (double)c->Bfull * c->world * T;  // B_g * T (Q7): all rows of all ranks
   LAUNCH(c, (ce_kernel<S><<<c->nblk_ce, 256, 0, c->stream>>>(n, B, (float)(1.0 / denom), 1)));
   LAUNCH(c, (ce_reduce_kernel<S><<<1, 256, 0, c->stream>>>(n, c->nblk_ce, 1)));
   phase(c, PH_DHDEC);
@@ -668,7 +673,10 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
       LAUNCH(c, (seg_finalize_kernel<S, 1><<<grid_for(5L * h * c->e), 256, 0, c->stream>>>(n, n.part, 1, 5 * h, c->e)));
     }
     LAUNCH(c, (db_kernel<S><<<grid_for(4L * h), 256, 0, c->stream>>>(n)));
+    if (c->nmb > 1) LAUNCH(c, (grad_accum_kernel<S><<<grid_for(c->P), 256, 0, c->stream>>>(n)));
   }
+  // persist this micro-batch's final (h, c) rows (TBTT state carry)
+  LAUNCH(c, (state_out_kernel<S><<<grid_for((long)B * h), 256, 0, c->stream>>>(n, MLSTM_SLOT_TRAIN)));
   return MLSTM_OK;
 }
 
@@ -684,7 +692,6 @@ mlstm_status enqueue_train_b(mlstm_ctx* c) {
   RET_IF(enqueue_transposes<S>(c));
   LAUNCH(c, (scaler_kernel<<<1, 1, 0, c->stream>>>(c->st, cf.scale_min, cf.scale_max, cf.scale_growth_interval,
                                                    cf.lr0, (long)cf.decay_iters)));
-  LAUNCH(c, (state_out_kernel<S><<<grid_for((long)c->B * c->h), 256, 0, c->stream>>>(n, MLSTM_SLOT_TRAIN)));
   return MLSTM_OK;
 }
 
@@ -725,19 +732,40 @@ mlstm_status build_graphs(mlstm_ctx* c) {
   return s;
 }
 
+void accumulate_phases(mlstm_ctx* c, int from, int to) {
+  float ms;
+  for (int p = from; p < to; ++p)
+    if (cudaEventElapsedTime(&ms, c->ev[p], c->ev[p + 1]) == cudaSuccess) c->phase_ms[p] += ms;
+}
+
+// One step: for each micro-batch, copy its rows of the input (host or device) into the step
+// buffers and run graph A (forward, BPTT, weight gradients, fp32 accumulation across micro-batches);
+// then the allreduce and graph B (overflow check, scaler, Adam, cast) once.
 template <typename S>
-mlstm_status run_train(mlstm_ctx* c) {
+mlstm_status run_train(mlstm_ctx* c, const uint8_t* bytes, const uint8_t* reset, cudaMemcpyKind kind) {
   if (!c->gA) RET_IF(build_graphs<S>(c));
   Net<S>& n = net<S>(c);
-  CUDA_OR_FAIL(c, cudaGraphLaunch(c->gA, c->stream));
+  const size_t rowb = (size_t)(c->T + 1);
+  for (int i = 0; i < c->nmb; ++i) {
+    set_microbatch_kernel<<<1, 1, 0, c->stream>>>(c->st, i);
+    CUDA_OR_FAIL(c, cudaGetLastError());
+    CUDA_OR_FAIL(c, cudaMemcpyAsync(c->bytes, bytes + (size_t)i * c->B * rowb, (size_t)c->B * rowb, kind, c->stream));
+    if (reset) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->reset, reset + (size_t)i * c->B, c->B, kind, c->stream));
+    else CUDA_OR_FAIL(c, cudaMemsetAsync(c->reset, 0, c->B, c->stream));
+    CUDA_OR_FAIL(c, cudaGraphLaunch(c->gA, c->stream));
+    if (c->profile) {
+      CUDA_OR_FAIL(c, cudaEventRecord(c->ev[PH_ALLREDUCE], c->stream));
+      if (i + 1 < c->nmb) {  // earlier micro-batches: fold their phase times in now
+        CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+        accumulate_phases(c, PH_PREP, PH_ALLREDUCE);
+      }
+    }
+  }
   if (c->world > 1) {
     c->cur_phase = PH_ALLREDUCE;
-    if (c->profile) CUDA_OR_FAIL(c, cudaEventRecord(c->ev[PH_ALLREDUCE], c->stream));
     NCCL_OR_FAIL(c, ncclAllReduce(n.arena, n.arena, (size_t)c->P, c->mixed ? ncclFloat16 : ncclFloat32, ncclSum,
                                   c->comm, c->stream));
     NCCL_OR_FAIL(c, ncclAllReduce(&c->st->loss_sum, &c->st->loss_sum, 1, ncclFloat64, ncclSum, c->comm, c->stream));
-  } else if (c->profile) {
-    CUDA_OR_FAIL(c, cudaEventRecord(c->ev[PH_ALLREDUCE], c->stream));
   }
   CUDA_OR_FAIL(c, cudaGraphLaunch(c->gB, c->stream));
   if (c->profile) CUDA_OR_FAIL(c, cudaEventRecord(c->ev[NPH], c->stream));
@@ -756,7 +784,7 @@ void fill_result(mlstm_ctx* c, mlstm_step_result* out) {
   c->last = s;
   c->have_last = true;
   if (!out) return;
-  const double denom = (double)c->B * c->world * c->T;
+  const double denom = (double)c->Bfull * c->world * c->T;
   out->loss_nats = s.loss_sum / denom;
   out->bpc = out->loss_nats / std::log(2.0);
   out->lr = s.lr_used;
@@ -769,15 +797,7 @@ void fill_result(mlstm_ctx* c, mlstm_step_result* out) {
 mlstm_status after_step(mlstm_ctx* c, mlstm_step_result* out) {
   CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
   fill_result(c, out);
-  if (c->profile) {
-    float ms;
-    int prev = PH_PREP;
-    for (int p = PH_PREP + 1; p <= NPH; ++p) {
-      CUDA_OR_FAIL(c, cudaEventElapsedTime(&ms, c->ev[prev], c->ev[p]));
-      c->phase_ms[prev] += ms;
-      prev = p;
-    }
-  }
+  if (c->profile) accumulate_phases(c, PH_PREP, NPH);
   const DevState& s = *c->st_host;
   if (!s.skipped && !std::isfinite(s.loss_sum)) {
     if (++c->nonfinite_run >= c->cfg.diverge_patience)
@@ -964,10 +984,8 @@ mlstm_status mlstm_train_step(mlstm_ctx* c, const uint8_t* bytes, const uint8_t*
                               mlstm_step_result* out) {
   RET_IF(ctx_ok(c));
   if (!bytes) return fail(MLSTM_EINVAL, "null bytes");
-  CUDA_OR_FAIL(c, cudaMemcpyAsync(c->bytes, bytes, (size_t)c->B * (c->T + 1), cudaMemcpyDeviceToDevice, c->stream));
-  if (reset) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->reset, reset, c->B, cudaMemcpyDeviceToDevice, c->stream));
-  else CUDA_OR_FAIL(c, cudaMemsetAsync(c->reset, 0, c->B, c->stream));
-  RET_IF(c->mixed ? run_train<__half>(c) : run_train<float>(c));
+  RET_IF(c->mixed ? run_train<__half>(c, bytes, reset, cudaMemcpyDeviceToDevice)
+                  : run_train<float>(c, bytes, reset, cudaMemcpyDeviceToDevice));
   if (flags & MLSTM_ASYNC) return MLSTM_OK;
   return after_step(c, out);
 }
@@ -976,10 +994,8 @@ mlstm_status mlstm_train_step_host(mlstm_ctx* c, const uint8_t* bytes_host, cons
                                    mlstm_step_result* out) {
   RET_IF(ctx_ok(c));
   if (!bytes_host) return fail(MLSTM_EINVAL, "null bytes");
-  CUDA_OR_FAIL(c, cudaMemcpyAsync(c->bytes, bytes_host, (size_t)c->B * (c->T + 1), cudaMemcpyHostToDevice, c->stream));
-  if (reset_host) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->reset, reset_host, c->B, cudaMemcpyHostToDevice, c->stream));
-  else CUDA_OR_FAIL(c, cudaMemsetAsync(c->reset, 0, c->B, c->stream));
-  RET_IF(c->mixed ? run_train<__half>(c) : run_train<float>(c));
+  RET_IF(c->mixed ? run_train<__half>(c, bytes_host, reset_host, cudaMemcpyHostToDevice)
+                  : run_train<float>(c, bytes_host, reset_host, cudaMemcpyHostToDevice));
   return after_step(c, out);
 }
 
@@ -991,6 +1007,8 @@ mlstm_status mlstm_eval(mlstm_ctx* c, const uint8_t* bytes, int32_t Be, const ui
   CUDA_OR_FAIL(c, cudaMemcpyAsync(c->bytes, bytes, (size_t)Be * (c->T + 1), cudaMemcpyDeviceToDevice, c->stream));
   CUDA_OR_FAIL(c, cudaMemsetAsync(c->reset, 0, c->B, c->stream));
   if (reset) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->reset, reset, Be, cudaMemcpyDeviceToDevice, c->stream));
+  set_microbatch_kernel<<<1, 1, 0, c->stream>>>(c->st, 0);
+  CUDA_OR_FAIL(c, cudaGetLastError());
   double nats = 0;
   RET_IF(c->mixed ? run_eval<__half>(c, Be, &nats) : run_eval<float>(c, Be, &nats));
   const int64_t tok = (int64_t)Be * c->T * c->world;
@@ -1050,7 +1068,7 @@ mlstm_status mlstm_get_grads(mlstm_ctx* c, float* host_out) {
 mlstm_status mlstm_get_state(mlstm_ctx* c, int slot, float* h_out, float* c_out) {
   RET_IF(ctx_ok(c));
   if (slot != 0 && slot != 1) return fail(MLSTM_EINVAL, "bad slot");
-  const long BH = (long)c->B * c->h;
+  const long BH = (long)c->Bfull * c->h;
   const size_t es = c->mixed ? 2 : 4;
   if (h_out) RET_IF(read_floats(c, (const uint8_t*)hstate_ptr(c) + es * slot * BH, BH, h_out));
   if (c_out) {
@@ -1063,7 +1081,7 @@ mlstm_status mlstm_get_state(mlstm_ctx* c, int slot, float* h_out, float* c_out)
 mlstm_status mlstm_set_state(mlstm_ctx* c, int slot, const float* h_in, const float* c_in) {
   RET_IF(ctx_ok(c));
   if (slot != 0 && slot != 1) return fail(MLSTM_EINVAL, "bad slot");
-  const long BH = (long)c->B * c->h;
+  const long BH = (long)c->Bfull * c->h;
   const size_t es = c->mixed ? 2 : 4;
   if (h_in) RET_IF(write_floats(c, (uint8_t*)hstate_ptr(c) + es * slot * BH, BH, h_in));
   if (c_in) {

@@ -46,12 +46,13 @@ struct DevState {
   int64_t it;          // LR clock: advances every step (incl. skipped)
   int64_t tau;         // applied Adam updates
   int32_t skipped;     // last step skipped?
-  int32_t pad;
+  int32_t mb;          // micro-batch index being processed (rows [mb*B, (mb+1)*B) of the rank's batch)
 };
 
 template <typename S>
 struct Net {
   int h, e, B, T, Bp;
+  int Bfull, nmb;  // rows per rank and micro-batches per step (B = Bfull / nmb rows per micro-batch)
   long ldK;  // leading dim of the transposed stashes over K = T*Bp (padded to 64)
   long ldH;  // leading dim of HT over (T+1)*Bp
   ParamOffsets po;
@@ -85,8 +86,9 @@ struct Net {
   S* dAT;         // [h][ldK]
   float* part;    // split-K partials
   float* Scan;    // [256][5h] per-byte segmented sums, canonical columns
-  S* hstate;      // [2][B][h]  persisted h per slot
-  float* cstate;  // [2][B][h]  persisted c per slot
+  S* hstate;      // [2][Bfull][h]  persisted h per slot
+  float* cstate;  // [2][Bfull][h]  persisted c per slot
+  float* gacc;    // [P] fp32 gradient accumulator across micro-batches (nmb > 1)
   double* loss_part;
   float* colsum_part;
   DevState* st;

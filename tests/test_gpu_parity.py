@@ -218,3 +218,29 @@ def test_host_entry_point_matches_device_entry_point():
     rb = b.train_step_host(by)
     assert ra == rb
     assert np.array_equal(a.get_params(), b.get_params())
+
+
+@pytest.mark.parametrize("precision", ["fp32", "mixed"])
+def test_micro_batches_equal_one_batch(precision):
+    """Micro-batching (4096 rows/GPU as 1024-row micro-batches) accumulates gradients in
+    fp32 across micro-batches: the step equals one un-split step on the same rows (fp32 mode to
+    fp32 rounding; mixed mode to the per-micro-batch fp16 rounding of the gradients), and the
+    persisted state of every row is carried."""
+    h, e, B, T = 128, 64, 12, 6
+    by0 = inputs(B, T, k=0)
+    by1 = inputs(B, T, k=1)
+    whole = make_model(h, e, B, T, precision)
+    split = make_model(h, e, B, T, precision, micro_batch=4)
+    for by in (by0, by1):
+        ra, rb = whole.train_step(to_dev(by)), split.train_step(to_dev(by))
+        assert abs(ra["loss_nats"] - rb["loss_nats"]) <= 1e-6 * ra["loss_nats"]
+        ga, gb = whole.get_grads().astype(np.float64), split.get_grads().astype(np.float64)
+        if precision == "fp32":
+            assert rel_l2(gb, ga) < 1e-5
+        else:
+            rep = compare_grads(gb, ga, h, e, "mixed")
+            assert min(rep.values()) > 0.9999, rep
+    ha, ca = whole.get_state(0)
+    hb, cb = split.get_state(0)
+    assert np.abs(ha - hb).max() < (1e-6 if precision == "fp32" else 2e-3)
+    assert rel_l2(split.get_params().astype(np.float64), whole.get_params().astype(np.float64)) < 1e-4
