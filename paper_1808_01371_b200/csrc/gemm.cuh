@@ -394,6 +394,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr int PIECE = WIDTH > 64 ? 64 : WIDTH;             // columns per epilogue call
   constexpr int NG = PIECE / 16;
   static_assert(WIDTH % PIECE == 0 && NG >= Epi::kMinGroups, "epilogue granularity");
+  // the cooperative tile epilogue stages the reduced slice (fp32) and its own scratch in the idle
+  // pipeline stages, which hold them only for 64-column slices; wider slices use the row epilogue
+  constexpr bool kUseTile = HasTile<Epi>::value && SLICE <= 64;
   extern __shared__ uint8_t smem_raw[];
   const SmemLayout<C> L(smem_raw);
   MLSTM_TRACE_BEGIN();
@@ -461,7 +464,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
         const int col0 = n0 + cl;
-        if constexpr (HasTile<Epi>::value) {
+        if constexpr (kUseTile) {
           float4* d = reinterpret_cast<float4*>(stageT + rl * (SLICE + 4) + (cl - z * SLICE));
 #pragma unroll
           for (int i = 0; i < PIECE / 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
@@ -471,7 +474,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
     if (tracing && threadIdx.x == 64) tr_ts[6] = ptx::globaltimer();
-    if constexpr (HasTile<Epi>::value) {
+    if constexpr (kUseTile) {
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (tracing && threadIdx.x == 64) tr_ts[7] = ptx::globaltimer();
       const int c0 = n0 + z * SLICE;

@@ -93,6 +93,14 @@ struct mlstm_ctx {
   Net<__half> nh{};
   Net<float> nf{};
   ncclComm_t comm = nullptr;
+  // N>1: the gradient allreduce runs on a high-priority stream in buckets that start as soon as
+  // the weight-gradient GEMM producing them finishes (W_h, then W_mh, then the rest), overlapping
+  // the remaining weight-gradient work; MLSTM_AR_OVERLAP=0 reduces after graph A.
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_wh = nullptr, ev_wmh = nullptr, ev_a_end = nullptr, ev_comm = nullptr;
+  bool ar_overlap = true;
+  int force_plan = 0;  // MLSTM_FORCE_PLAN (test instrument), applied while this ctx enqueues
+  bool overlap_now() const { return world > 1 && ar_overlap && nmb == 1; }
   cudaGraphExec_t gA = nullptr, gB = nullptr;
   std::map<std::tuple<const void*, long, long, long, long, long, int>, CUtensorMap> maps;
   mlstm_status failed = MLSTM_OK;
@@ -160,18 +168,33 @@ int grid_for(long n, int threads = 256, int cap = 148 * 16) {
 // (256 x 256 per pair) halves per-SM operand traffic and wins whenever it can fill ~60 pairs,
 // with split-K where allowed.  Otherwise one CTA per 128-row tile with the widest BN that still
 // fills ~120 SMs.
+// Test instrument (MLSTM_FORCE_PLAN=pair|split|single): take one tile plan wherever it is legal, so
+// small parity tests cover the plans that only full-size shapes select on their own.
+int g_force_plan = 0;
+
 Plan plan_gemm(bool tc, long M, long N, long K, bool allow_split) {
   Plan p{64, 1, false, false};
   const long kb = (K + 63) / 64;
+  if (tc && g_force_plan == 1 && M > 128) return Plan{256, 1, true, false};
+  if (tc && g_force_plan == 2 && kb >= 8) {
+    const int sp = kb >= 16 ? 4 : 2;
+    if (((M + 127) / 128) * ((N + 255) / 256) * sp <= 160) return Plan{256, sp, false, true};
+  }
+  if (tc && g_force_plan == 3) allow_split = false;
+  if (tc && g_force_plan != 0) goto single;
   if (tc && M > 128 && ((M + 255) / 256) * ((N + 255) / 256) >= 60) return Plan{256, 1, true, false};
-  const long mt = (M + 127) / 128;
   if (tc) {
+    const long mt = (M + 127) / 128;
     // 128 x 256 tiles with the K loop split over a cluster of S <= 4 CTAs when 256-wide tiles
     // alone cannot fill the GPU (measured: N=64 tiles issue MMAs at ~1/4 of the N=256 rate)
     const long tiles = mt * ((N + 255) / 256);
     int sp = 1;
     while (tiles * sp < 100 && sp < 4 && kb / (sp * 2) >= 4) sp *= 2;
     if (sp > 1 && tiles * sp <= 160) return Plan{256, sp, false, true};
+  }
+single:
+  if (tc) {
+    const long mt = (M + 127) / 128;
     for (int bn : {256, 128, 64}) {
       if (mt * ((N + bn - 1) / bn) >= 120 || bn == 64) {
         p.bn = bn;
@@ -180,7 +203,7 @@ Plan plan_gemm(bool tc, long M, long N, long K, bool allow_split) {
     }
   }
   if (allow_split) {
-    const long tiles = mt * ((N + p.bn - 1) / p.bn);
+    const long tiles = ((M + 127) / 128) * ((N + p.bn - 1) / p.bn);
     while (tiles * p.splits < 148 && kb / (p.splits * 2) >= 4) p.splits *= 2;
   }
   return p;
@@ -294,6 +317,12 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   if (const char* v = getenv("MLSTM_PF_BWD")) c->pf_bwd = (float)atof(v);
   if (const char* v = getenv("MLSTM_PF_STASH")) c->pf_stash = v[0] != '0';
   if (const char* v = getenv("MLSTM_L2_WH")) c->l2_wh = (float)atof(v);
+  if (const char* v = getenv("MLSTM_AR_OVERLAP")) c->ar_overlap = v[0] != '0';
+  {
+    const char* v = getenv("MLSTM_FORCE_PLAN");
+    const std::string fp = v ? v : "";
+    c->force_plan = fp == "pair" ? 1 : fp == "split" ? 2 : fp == "single" ? 3 : 0;
+  }
   const char* dbg = getenv("MLSTM_DEBUG_SIMT_GEMM");  // test instrument: mixed mode on the SIMT engine
   c->tc = c->mixed && !(dbg && dbg[0] == '1');
 }
@@ -400,6 +429,8 @@ cudaError_t launch_tc1s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* 
                         int bz, uint32_t pa, uint32_t pb, int flags, PrefetchJob pj,
                         const Epi& epi) {
   const int kb = (K + 63) / 64, kbps = (kb + S - 1) / S;
+  if ((long)S * ((N + 255) / 256) * ((M + 127) / 128) * 128 * 256 > kSplitScratchFloats)
+    return cudaErrorInvalidConfiguration;  // the split-K partials would not fit the scratch
   return launch_gemm(c, gemm_tc1s_kernel<S, Epi>, dim3(S * ((N + 255) / 256), (M + 127) / 128, 1), TcCfg<256>::SMEM,
                      S, *ma, *mb, *ma2, *mb2, sg, M, N, K, az, bz, kbps, pa, pb, flags, pj, c->split_scratch, epi);
 }
@@ -651,7 +682,8 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
         {{n.OHT, 256, Kt, c->ldK, 1, 256 * c->ldK}, {n.dGT, 5L * h, Kt, c->ldK, 1, 5L * h * c->ldK}, 256, 5L * h,
          0, 2},                                                                        // S = onehot^T [dMX|dZ]
     };
-    for (const W& w : ws) {
+    for (int wi = 0; wi < 4; ++wi) {
+      const W& w = ws[wi];
       const Plan p = plan_gemm(c->tc, w.M, w.N, Kt, true);
       if (p.splits == 1 || p.pair || p.cluster) {
         RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kt, p, EpiWgrad<S>{n, w.off, w.mode, (int)w.N}));
@@ -660,6 +692,9 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
         LAUNCH(c, (wgrad_finalize_kernel<S><<<grid_for(w.M * w.N), 256, 0, c->stream>>>(n, n.part, p.splits, (int)w.M,
                                                                                           (int)w.N, w.off, w.mode)));
       }
+      // bucket boundaries of the overlapped allreduce (external event nodes in the graph)
+      if (c->overlap_now() && wi < 2)
+        CUDA_OR_FAIL(c, cudaEventRecordWithFlags(wi == 0 ? c->ev_wh : c->ev_wmh, c->stream, cudaEventRecordExternal));
     }
     // dE = S [W_mx; W_x] (M=256, N=e, K=5h) and [dW_mx; dW_x] = S^T E (M=5h, N=e, K=256)
     {
@@ -723,12 +758,14 @@ mlstm_status build_graphs(mlstm_ctx* c) {
   if (c->gA) cudaGraphExecDestroy(c->gA);
   if (c->gB) cudaGraphExecDestroy(c->gB);
   c->gA = c->gB = nullptr;
+  g_force_plan = c->force_plan;
   c->counting = true;
   c->launches = 0;
   memset(c->phase_launches, 0, sizeof c->phase_launches);
   mlstm_status s = record_graph<S>(c, enqueue_train_a<S>, &c->gA);
   if (s == MLSTM_OK) s = record_graph<S>(c, enqueue_train_b<S>, &c->gB);
   c->counting = false;
+  g_force_plan = 0;
   return s;
 }
 
@@ -763,9 +800,30 @@ mlstm_status run_train(mlstm_ctx* c, const uint8_t* bytes, const uint8_t* reset,
   }
   if (c->world > 1) {
     c->cur_phase = PH_ALLREDUCE;
-    NCCL_OR_FAIL(c, ncclAllReduce(n.arena, n.arena, (size_t)c->P, c->mixed ? ncclFloat16 : ncclFloat32, ncclSum,
-                                  c->comm, c->stream));
-    NCCL_OR_FAIL(c, ncclAllReduce(&c->st->loss_sum, &c->st->loss_sum, 1, ncclFloat64, ncclSum, c->comm, c->stream));
+    const ncclDataType_t dt = c->mixed ? ncclFloat16 : ncclFloat32;
+    if (c->overlap_now()) {
+      // fp16 SUM in three buckets on the comm stream; bucket k waits for the GEMM that wrote it
+      const ParamOffsets& po = c->po;
+      S* a = n.arena;
+      cudaStream_t cs = c->comm_stream;
+      CUDA_OR_FAIL(c, cudaEventRecord(c->ev_a_end, c->stream));
+      CUDA_OR_FAIL(c, cudaStreamWaitEvent(cs, c->ev_wh, 0));
+      NCCL_OR_FAIL(c, ncclAllReduce(a + po.Wh, a + po.Wh, (size_t)(po.b - po.Wh), dt, ncclSum, c->comm, cs));
+      CUDA_OR_FAIL(c, cudaStreamWaitEvent(cs, c->ev_wmh, 0));
+      NCCL_OR_FAIL(c, ncclAllReduce(a + po.Wmh, a + po.Wmh, (size_t)(po.Wx - po.Wmh), dt, ncclSum, c->comm, cs));
+      CUDA_OR_FAIL(c, cudaStreamWaitEvent(cs, c->ev_a_end, 0));
+      NCCL_OR_FAIL(c, ncclGroupStart());
+      NCCL_OR_FAIL(c, ncclAllReduce(a, a, (size_t)po.Wmh, dt, ncclSum, c->comm, cs));
+      NCCL_OR_FAIL(c, ncclAllReduce(a + po.Wx, a + po.Wx, (size_t)(po.Wh - po.Wx), dt, ncclSum, c->comm, cs));
+      NCCL_OR_FAIL(c, ncclAllReduce(a + po.b, a + po.b, (size_t)(po.P - po.b), dt, ncclSum, c->comm, cs));
+      NCCL_OR_FAIL(c, ncclAllReduce(&c->st->loss_sum, &c->st->loss_sum, 1, ncclFloat64, ncclSum, c->comm, cs));
+      NCCL_OR_FAIL(c, ncclGroupEnd());
+      CUDA_OR_FAIL(c, cudaEventRecord(c->ev_comm, cs));
+      CUDA_OR_FAIL(c, cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
+    } else {
+      NCCL_OR_FAIL(c, ncclAllReduce(n.arena, n.arena, (size_t)c->P, dt, ncclSum, c->comm, c->stream));
+      NCCL_OR_FAIL(c, ncclAllReduce(&c->st->loss_sum, &c->st->loss_sum, 1, ncclFloat64, ncclSum, c->comm, c->stream));
+    }
   }
   CUDA_OR_FAIL(c, cudaGraphLaunch(c->gB, c->stream));
   if (c->profile) CUDA_OR_FAIL(c, cudaEventRecord(c->ev[NPH], c->stream));
@@ -811,7 +869,10 @@ mlstm_status after_step(mlstm_ctx* c, mlstm_step_result* out) {
 template <typename S>
 mlstm_status run_eval(mlstm_ctx* c, int Be, double* nats) {
   Net<S>& n = net<S>(c);
-  RET_IF(enqueue_forward<S>(c, MLSTM_SLOT_EVAL));
+  g_force_plan = c->force_plan;
+  const mlstm_status fs = enqueue_forward<S>(c, MLSTM_SLOT_EVAL);
+  g_force_plan = 0;
+  RET_IF(fs);
   LAUNCH(c, (ce_kernel<S><<<c->nblk_ce, 256, 0, c->stream>>>(n, Be, 0.f, 0)));
   LAUNCH(c, (ce_reduce_kernel<S><<<1, 256, 0, c->stream>>>(n, c->nblk_ce, 0)));
   LAUNCH(c, (state_out_kernel<S><<<grid_for((long)c->B * c->h), 256, 0, c->stream>>>(n, MLSTM_SLOT_EVAL)));
@@ -975,6 +1036,13 @@ mlstm_status mlstm_init(const mlstm_config* cfg, void* workspace, size_t workspa
     memcpy(&id, nccl_id, 128);
     ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
     if (r != ncclSuccess) return bail(fail(MLSTM_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)));
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi) != cudaSuccess)
+      return bail(fail(MLSTM_ECUDA, "cudaStreamCreateWithPriority"));
+    for (cudaEvent_t* ev : {&c->ev_wh, &c->ev_wmh, &c->ev_a_end, &c->ev_comm})
+      if (cudaEventCreateWithFlags(ev, cudaEventDisableTiming) != cudaSuccess)
+        return bail(fail(MLSTM_ECUDA, "cudaEventCreate"));
   }
   *out = c;
   return MLSTM_OK;
@@ -1330,6 +1398,9 @@ void mlstm_destroy(mlstm_ctx* c) {
   if (c->st_host) cudaFreeHost(c->st_host);
   if (c->cap) cudaStreamDestroy(c->cap);
   if (c->comm) ncclCommDestroy(c->comm);
+  for (cudaEvent_t ev : {c->ev_wh, c->ev_wmh, c->ev_a_end, c->ev_comm})
+    if (ev) cudaEventDestroy(ev);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   delete c;
 }
 

@@ -69,19 +69,25 @@ def test_train_step_parity(name, h, e, B, T, precision):
 
 
 def test_multi_step_trace_fp32_tracks_oracle():
-    """10 steps (forward, BPTT, scaler, Adam, schedule, persisted state) vs the oracle loop."""
+    """100 steps (forward, BPTT, scaler, Adam, schedule, persisted state) vs the oracle loop
+    (SURVEY 8(d) C4 validation (i): fp32-mode loss trace within rel 1e-3 per step; first 10 steps 1e-4)."""
     h, e, B, T = 64, 64, 4, 16
     m = make_model(h, e, B, T, "fp32")
     st = O.new_train_state(h, e, B, seed=0x5EED)
     assert np.array_equal(st.theta.astype(np.float32), m.get_params())
-    for k in range(10):
+    worst = 0.0
+    for k in range(100):
         by = inputs(B, T, k=k)
         r = m.train_step(to_dev(by))
         ro = O.train_step(st, by)
-        assert abs(r["loss_nats"] - ro["loss_nats"]) <= 1e-4 * ro["loss_nats"], (k, r, ro)
+        rel = abs(r["loss_nats"] - ro["loss_nats"]) / ro["loss_nats"]
+        worst = max(worst, rel)
+        assert rel <= (1e-4 if k < 10 else 1e-3), (k, r, ro)
         assert r["lr"] == pytest.approx(ro["lr"], rel=1e-12) and r["loss_scale"] == ro["alpha"]
         assert bool(r["skipped"]) == ro["skipped"]
-    assert rel_l2(m.get_params().astype(np.float64), st.theta) < 1e-4
+        if k == 9:
+            assert rel_l2(m.get_params().astype(np.float64), st.theta) < 1e-4
+    assert rel_l2(m.get_params().astype(np.float64), st.theta) < 1e-3, worst
 
 
 @pytest.mark.parametrize("precision", ["fp32", "mixed"])
@@ -244,3 +250,25 @@ def test_micro_batches_equal_one_batch(precision):
     hb, cb = split.get_state(0)
     assert np.abs(ha - hb).max() < (1e-6 if precision == "fp32" else 2e-3)
     assert rel_l2(split.get_params().astype(np.float64), whole.get_params().astype(np.float64)) < 1e-4
+
+
+@pytest.mark.parametrize("plan", ["pair", "split", "single"])
+@pytest.mark.parametrize("h,B,T", [(512, 256, 4), (512, 200, 3), (1024, 256, 2)])
+def test_forced_tile_plans_match_oracle(plan, h, B, T, monkeypatch):
+    """Every tcgen05 tile plan (CTA pair, cluster split-K, single CTA) on every GEMM of the step,
+    forced at a size the oracle finishes quickly (full-size shapes select them on their own);
+    B=200 leaves a ragged last M tile."""
+    monkeypatch.setenv("MLSTM_FORCE_PLAN", plan)
+    e = 64
+    m = make_model(h, e, B, T, "mixed")
+    theta0 = m.get_params().astype(np.float64)
+    by = inputs(B, T)
+    res = m.train_step(to_dev(by))
+    loss_ref, g_ref, (hT, cT), _ = oracle_step(theta0, by, h, e)
+    assert abs(res["loss_nats"] - loss_ref) / loss_ref <= TOL["mixed"]["loss_rel"]
+    rep = compare_grads(m.get_grads().astype(np.float64), g_ref, h, e, "mixed")
+    assert min(rep.values()) >= TOL["mixed"]["grad_cos"], rep
+    hs, cs = m.get_state(0)
+    assert np.abs(hs - hT).max() <= 2e-3 and np.abs(cs - cT).max() <= 2e-2
+    nats, tokens, _ = m.eval(to_dev(inputs(B, T, k=1)))
+    assert np.isfinite(nats) and tokens == B * T

@@ -6,7 +6,8 @@ import torch
 import paper_1808_01371_b200 as M
 torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False
 shapes = [("F2", 256, 16384, 4096), ("F1/B2", 256, 4096, 4096), ("B1", 256, 4096, 16384),
-          ("dW_h", 16384, 4096, 65536), ("dW_mh", 4096, 4096, 65536), ("sq8192", 8192, 8192, 8192)]
+          ("dW_h", 16384, 4096, 65536), ("dW_mh", 4096, 4096, 65536), ("sq8192", 8192, 8192, 8192),
+          ("F2@1k", 1024, 16384, 4096), ("F1@1k", 1024, 4096, 4096), ("B1@1k", 1024, 4096, 16384)]
 for name, m, n, k in shapes:
     it = 3 if m * n * k > 1e12 else 20
     ours = M.mlstm_gemm_bench(3, m, n, k, 0, it)
