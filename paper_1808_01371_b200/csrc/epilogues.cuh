@@ -254,7 +254,7 @@ __device__ __forceinline__ void b2_tile(const Net<S>& n, int s, const float* T, 
         const int r = min(rb + k * rpi, rows - 1);
         const long row = (long)s * n.B + m0 + r;
         const float4 t4 = *reinterpret_cast<const float4*>(T + r * ldt + u0);
-        const float4 d4 = ld4(n.dHdec + row * h + j);
+        const float4 d4 = n.dHdec ? ld4(n.dHdec + row * h + j) : make_float4(0.f, 0.f, 0.f, 0.f);
         dh[k] = make_float4(t4.x + d4.x, t4.y + d4.y, t4.z + d4.z, t4.w + d4.w);
         const S* g = n.Gates + row * 4 * h + gcol;
         gi[k] = ld4(g);
@@ -327,13 +327,14 @@ struct EpiB2 {
   }
   template <int NG>
   __device__ __forceinline__ void run(int b, int col0, const float* v) const {
-    const float* dhd = n.dHdec + ((long)s * n.B + b) * n.h + col0;
+    // dH = dH_rec + dH_dec; on the tcgen05 path dH_dec is already in the accumulator (dHdec null)
+    const float* dhd = n.dHdec ? n.dHdec + ((long)s * n.B + b) * n.h + col0 : nullptr;
 #pragma unroll
     for (int q = 0; q < NG; ++q) {
       float dh[16];
-      ld16(dhd + 16 * q, dh);
+      if (dhd) ld16(dhd + 16 * q, dh);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) dh[i] += v[16 * q + i];
+      for (int i = 0; i < 16; ++i) dh[i] = (dhd ? dh[i] : 0.f) + v[16 * q + i];
       gate_bwd16(n, s, b, col0 + 16 * q, dh);
     }
   }

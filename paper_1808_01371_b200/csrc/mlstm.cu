@@ -247,7 +247,8 @@ void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
   n.dY = cv.take<S>((long)T * B * 256);
   n.dYT = cv.take<S>(256L * c->ldK);
   n.OHT = cv.take<S>(256L * c->ldK);
-  n.dHdec = cv.take<float>((long)T * B * h);
+  // tcgen05 path: dH_dec,t = dY_t W_dec enters the B2 accumulator as a second K segment (no buffer)
+  n.dHdec = c->tc ? nullptr : cv.take<float>((long)T * B * h);
   n.dZscr = cv.take<S>((long)B * 4 * h);
   n.dAscr = cv.take<S>((long)B * h);
   n.dC = cv.take<float>((long)B * h);
@@ -257,10 +258,12 @@ void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
   long part = 64;
   const long K = c->Kt;
   const long shapes[4][2] = {{4L * h, h}, {h, h}, {256, h}, {256, 5L * h}};
+  g_force_plan = c->force_plan;  // size for the plans this ctx will take
   for (auto& s : shapes) {
     Plan p = plan_gemm(c->tc, s[0], s[1], K, true);
     if (p.splits > 1 && !p.pair && !p.cluster) part = std::max(part, (long)p.splits * s[0] * s[1]);
   }
+  g_force_plan = 0;
   c->seg_splits = (int)std::max(1L, std::min(64L, (5L * h) / 512));
   part = std::max(part, (long)c->seg_splits * 256 * e);
   part = std::max(part, 5L * h * e);
@@ -633,13 +636,24 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
   LAUNCH(c, (ce_kernel<S><<<c->nblk_ce, 256, 0, c->stream>>>(n, B, (float)(1.0 / denom), 1)));
   LAUNCH(c, (ce_reduce_kernel<S><<<1, 256, 0, c->stream>>>(n, c->nblk_ce, 1)));
   phase(c, PH_DHDEC);
-  {
+  const Opd dYs{n.dY, B, 256, 256, T, (long)B * 256, kPolFirst};  // dY_s = rows of timestep s
+  const Opd WdecT{n.WdecT, h, 256, 256, 1, 256L * h, 0, true};
+  if (n.dHdec) {  // SIMT path: dH_dec for all timesteps in one GEMM
     Opd A{n.dY, (long)T * B, 256, 256, 1, (long)T * B * 256};
-    Opd Bo{n.WdecT, h, 256, 256, 1, 256L * h, 0, true};
-    RET_IF(gemm<S>(c, A, 0, Bo, 0, T * B, h, 256, plan_gemm(c->tc, (long)T * B, h, 256, false), EpiDHdec<S>{n}));
+    RET_IF(gemm<S>(c, A, 0, WdecT, 0, T * B, h, 256, plan_gemm(c->tc, (long)T * B, h, 256, false), EpiDHdec<S>{n}));
   }
   phase(c, PH_BWD);
-  LAUNCH(c, (gate_bwd_last_kernel<S><<<grid_for((long)B * h / 16), 256, 0, c->stream>>>(n)));
+  if (n.dHdec) {
+    LAUNCH(c, (gate_bwd_last_kernel<S><<<grid_for((long)B * h / 16), 256, 0, c->stream>>>(n)));
+  } else {  // gate backward of the last timestep: dH = dY_{T-1} W_dec only (TBTT: no recurrent term)
+    RET_IF(gemm<S>(c, dYs, T - 1, WdecT, 0, B, h, 256, plan_gemm(c->tc, B, h, 256, false), EpiB2<S>{n, T - 1}));
+  }
+  Segment segd;  // B2's second K segment: + dY_{t-1} W_dec
+  if (!n.dHdec) {
+    segd.A2 = &dYs;
+    segd.B2 = &WdecT;
+    segd.K2 = 256;
+  }
   {
     const Opd dZ{n.dZscr, B, 4L * h, 4L * h, 1, 4L * B * h, kPolFirst};
     const Opd WhT{n.WhT, h, 4L * h, 4L * h, 1, 4L * h * h, pol_last(c->l2_wh), true};
@@ -657,12 +671,13 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
         const long BH = (long)B * h;
         pb1.add(n.Gates + (long)(t - 1) * 4 * BH, 4 * BH * (long)es);
         pb1.add(n.Crm + (long)(t - 1) * BH, 2 * BH * 4L);
-        pb1.add(n.dHdec + (long)(t - 1) * BH, BH * 4L);
+        if (n.dHdec) pb1.add(n.dHdec + (long)(t - 1) * BH, BH * 4L);
         pb2.add(n.Astash + (long)(t - 1) * BH, BH * (long)es);
       }
       if (c->pf_bwd > 0 && c->tc) pb2.add(n.WhT, (long)(c->pf_bwd * 8.0 * h * h));
       RET_IF(gemm<S>(c, dZ, 0, WhT, 0, B, h, 4 * h, p1, EpiB1<S>{n, t}, pb1));
-      if (t > 0) RET_IF(gemm<S>(c, dA, 0, WmhT, 0, B, h, h, p2, EpiB2<S>{n, t - 1}, pb2));
+      segd.az2 = t - 1;
+      if (t > 0) RET_IF(gemm<S>(c, dA, 0, WmhT, 0, B, h, h, p2, EpiB2<S>{n, t - 1}, pb2, segd));
     }
   }
   phase(c, PH_WGRAD);

@@ -78,7 +78,7 @@ struct Net {
   S* dY;          // [T*B][256]
   S* dYT;         // [256][ldK]
   S* OHT;         // [256][ldK] one-hot of the input bytes, transposed
-  float* dHdec;   // [T*B][h]
+  float* dHdec;   // [T*B][h] (SIMT path only; null when B2 folds dY W_dec into its K loop)
   S* dZscr;       // [B][4h] internal order
   S* dAscr;       // [B][h]
   float* dC;      // [B][h] dc carry

@@ -3,6 +3,7 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
 {
 timeout 600 python -m pytest tests/test_gpu_dp.py -q -x 2>&1 | tail -5
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k forced 2>&1 | tail -5
 for ov in 1 0 1; do
   echo "== MLSTM_AR_OVERLAP=$ov C3"
   MLSTM_AR_OVERLAP=$ov timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 10 --warmup 3 --no-e2e
