@@ -291,8 +291,15 @@ def main():
     dom_ms = gem[dom][0] / args.steps
     dom_launches = gem[dom][1]
     achieved = pf[dom] / (dom_ms / 1e3) / 1e12
+    traffic = None
+    try:  # measured DRAM bytes per launch of this phase's kernels (committed ncu capture)
+        tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")))
+        traffic = tj.get(args.config, {}).get(dom, {}).get("bytes_per_launch")
+    except (OSError, ValueError):
+        pass
     roof = {"bound": "tensor", "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
-            "frac": achieved / sustained, "traffic": None, "peak_source": f"{src} bf16_tflops_sustained",
+            "frac": achieved / sustained, "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
+            "peak_source": f"{src} bf16_tflops_sustained",
             "kernel": f"gemm_tc_kernel ({dom} phase: {dom_launches} launches/step, "
                       f"{pf[dom] / dom_launches / 1e9:.2f} GFLOP per launch avg, "
                       f"{dom_ms / dom_launches * 1e3:.1f} us per launch avg)"}

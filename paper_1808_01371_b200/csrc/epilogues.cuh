@@ -113,6 +113,100 @@ struct EpiF2 {  // one call = 4 gates x 16 units: NG must be 4
   }
 };
 
+// Async-I/O form of EpiF2 (tcgen05 engines; W_x x + b always folded there).  Per warp and slot
+// (one 64-column call): c_{t-1} rows come in by bulk copy; gates, c_t and h_t rows are staged in
+// the warp's window with 16-byte row padding (conflict-free) and leave by bulk copy.
+// Warp-cooperative store of 32 staged rows (row r of the warp at src + r*spitch, `bytes` per row)
+// to dst + r*dpitch (elements of 16 bytes): consecutive lanes take consecutive 16-byte pieces of a
+// row, so one warp instruction writes 512/bytes full rows instead of touching 32 lines.
+__device__ __forceinline__ void warp_rows_out(uint8_t* dst, long dpitch, const uint8_t* src, int spitch, int bytes,
+                                              int nvalid, int lane) {
+  const int per = bytes >> 4;
+  __syncwarp();
+  for (int k = lane; k < 32 * per; k += 32) {
+    const int r = k / per, i = k - r * per;
+    if (r < nvalid)
+      *reinterpret_cast<uint4*>(dst + r * dpitch + i * 16) = *reinterpret_cast<const uint4*>(src + r * spitch + i * 16);
+  }
+}
+
+template <typename S>
+struct EpiF2IO : EpiF2<S> {
+  static constexpr bool kAsyncIO = true;
+  int out_mode;  // 1: per-row bulk copies out; 2: warp-cooperative coalesced stores
+  static constexpr int kCp = 0, kG = 32 * 80, kC = kG + 32 * 144, kH = kC + 32 * 80, kSlot = kH + 32 * 48;
+  static_assert(2 * kSlot <= kWarpStageBytes, "staging window");
+  __device__ __forceinline__ void io_issue(const EpiIO& io, int slot, int col0) const {
+    const Net<S>& n = this->n;
+    if (!io.valid()) return;
+    const int b = io.row0 + io.lane, j0 = (col0 >> 6) * 16;
+    ptx::mbar_expect_tx(io.bar, 64);
+    ptx::bulk_g2s(io.buf + slot * kSlot + kCp + io.lane * 80, n.Crm + ((long)this->t * n.B + b) * n.h + j0, 64,
+                  io.bar);
+  }
+  template <int NG>
+  __device__ __forceinline__ void run_io(const EpiIO& io, int slot, int col0, const float* v) const {
+    static_assert(NG == 4, "one call = 4 gates x 16 units");
+    const Net<S>& n = this->n;
+    const int h = n.h, t = this->t, j0 = (col0 >> 6) * 16, lane = io.lane;
+    const int b = io.row0 + lane;
+    uint8_t* sb = io.buf + slot * kSlot;
+    ptx::mbar_wait(io.bar, 0);
+    const float4* cp = reinterpret_cast<const float4*>(sb + kCp + lane * 80);
+    __align__(16) S gs[64];
+    __align__(16) float cv[16];
+    __align__(16) S hv[16];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 c4 = cp[k];
+      const float cpv[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int jj = 4 * k + e;
+        const float gi = act_sigmoid<S>(v[jj]), gf = act_sigmoid<S>(v[16 + jj]);
+        const float go = act_sigmoid<S>(v[32 + jj]), gu = act_tanh<S>(v[48 + jj]);
+        gs[jj] = to_s<S>(gi);
+        gs[16 + jj] = to_s<S>(gf);
+        gs[32 + jj] = to_s<S>(go);
+        gs[48 + jj] = to_s<S>(gu);
+        cv[jj] = gf * cpv[e] + gi * gu;               // c_t = f c_{t-1} + i u   (fp32)
+        hv[jj] = to_s<S>(go * act_tanh<S>(cv[jj]));  // h_t = o tanh(c_t)
+      }
+    }
+    uint4* sg = reinterpret_cast<uint4*>(sb + kG + lane * 144);
+    uint4* sc = reinterpret_cast<uint4*>(sb + kC + lane * 80);
+    uint4* sh = reinterpret_cast<uint4*>(sb + kH + lane * 48);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sg[k] = reinterpret_cast<const uint4*>(gs)[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sc[k] = reinterpret_cast<const uint4*>(cv)[k];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) sh[k] = reinterpret_cast<const uint4*>(hv)[k];
+    if (out_mode == 1) {
+      ptx::fence_proxy_async_smem();
+      if (io.valid()) {
+        ptx::bulk_s2g(n.Gates + ((long)t * n.B + b) * 4 * h + col0, sg, 128);
+        ptx::bulk_s2g(n.Crm + ((long)(t + 1) * n.B + b) * h + j0, sc, 64);
+        ptx::bulk_s2g(n.Hrm + ((long)(t + 1) * n.B + b) * h + j0, sh, 32);
+      }
+      ptx::bulk_commit();
+    } else {
+      const int b0 = io.row0;
+      warp_rows_out(reinterpret_cast<uint8_t*>(n.Gates + ((long)t * n.B + b0) * 4 * h + col0), 8L * h, sb + kG, 144,
+                    128, io.nvalid, lane);
+      warp_rows_out(reinterpret_cast<uint8_t*>(n.Crm + ((long)(t + 1) * n.B + b0) * h + j0), 4L * h, sb + kC, 80, 64,
+                    io.nvalid, lane);
+      warp_rows_out(reinterpret_cast<uint8_t*>(n.Hrm + ((long)(t + 1) * n.B + b0) * h + j0), 2L * h, sb + kH, 48, 32,
+                    io.nvalid, lane);
+    }
+    if (io.valid()) {
+      const long kc = n.kcol(t + 1, b);
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) n.HT[(long)(j0 + jj) * n.ldH + kc] = hv[jj];
+    }
+  }
+};
+
 // (d) decoder logits Y = H W_dec^T + b_dec, fp32 ("operating on FP32 logits").
 template <typename S>
 struct EpiY {

@@ -16,6 +16,7 @@
 //   -> tcgen05.ld by the epilogue warps.  Measured engine choice: profiles/r01_gemm_sweep.log.
 // SIMT engine (fp32 parity mode, "single precision"): plain FFMA, 128 x 64 tile.
 #pragma once
+#include "net.cuh"
 #include "ptx.cuh"
 
 namespace mlstm {
@@ -56,6 +57,15 @@ struct HasTile<E, decltype(void(E::kTile))> {
   static constexpr bool value = E::kTile;
 };
 
+template <class E, class = void>
+struct HasAsyncIO {
+  static constexpr bool value = false;
+};
+template <class E>
+struct HasAsyncIO<E, decltype(void(E::kAsyncIO))> {
+  static constexpr bool value = E::kAsyncIO;
+};
+
 template <int BN>
 struct TcCfg {  // one CTA per 128 x BN tile
   static constexpr int BM = 128, BK = 64;
@@ -63,7 +73,8 @@ struct TcCfg {  // one CTA per 128 x BN tile
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512;
+  static_assert(STAGES * STAGE_BYTES >= kEpiWarps * kWarpStageBytes, "epilogue staging windows");
 };
 template <int BN>
 struct Tc2Cfg {  // CTA pair per 256 x BN tile: per CTA 128 rows of A, BN/2 rows of B
@@ -72,14 +83,15 @@ struct Tc2Cfg {  // CTA pair per 256 x BN tile: per CTA 128 rows of A, BN/2 rows
   static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = BN == 256 ? 6 : (BN == 128 ? 8 : 10);
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512;
+  static_assert(STAGES * STAGE_BYTES >= kEpiWarps * kWarpStageBytes, "epilogue staging windows");
 };
 
 // Shared-memory carve-up common to the tcgen05 kernels.
 template <class C>
 struct SmemLayout {
   uint8_t *sA, *sB;
-  uint64_t *full, *empty, *accf;
+  uint64_t *full, *empty, *accf, *epibar;
   uint32_t* tmem_slot;
   __device__ __forceinline__ explicit SmemLayout(uint8_t* smem_raw) {
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -89,6 +101,10 @@ struct SmemLayout {
     empty = full + C::STAGES;
     accf = empty + C::STAGES;
     tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+    epibar = accf + 2;  // kEpiWarps epilogue load barriers
+  }
+  __device__ __forceinline__ EpiIO io(int ew, int row0, int M, int lane) const {
+    return EpiIO{sA + ew * kWarpStageBytes, epibar + ew, row0, max(0, min(32, M - row0)), lane};
   }
 };
 
@@ -104,6 +120,8 @@ __device__ __forceinline__ void gemm_setup(const SmemLayout<C>& L, const CUtenso
       ptx::mbar_init(&L.empty[s], 1);  // the MMA commit (multicast to both CTAs in PAIR mode)
     }
     ptx::mbar_init(L.accf, 1);
+#pragma unroll 1
+    for (int w = 0; w < kEpiWarps; ++w) ptx::mbar_init(&L.epibar[w], 32);
     ptx::fence_barrier_init();
   }
   if (warp == 1) {
@@ -300,13 +318,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else {
     const int q = warp & 3, grp = (warp - 2) >> 2;
     const int row = m0 + q * 32 + lane;
-    epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
+    if constexpr (HasAsyncIO<Epi>::value) {
+      const EpiIO io = L.io(warp - 2, m0 + q * 32, M, lane);
+      epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
+      for (int c = grp, slot = 0; c < BN / 64; c += 2, ++slot)
+        if (n0 + c * 64 < N) epi.io_issue(io, slot, n0 + c * 64);
+      ptx::mbar_arrive(io.bar);
 #pragma unroll 1
-    for (int c = grp; c < BN / 64; c += 2) {
-      float v[64];
-      tmem_chunk(tmem, q, c, nkb > 0, v);
-      const int col0 = n0 + c * 64;
-      if (row < M && col0 < N) epi.template run<4>(row, col0, v);
+      for (int c = grp, slot = 0; c < BN / 64; c += 2, ++slot) {
+        float v[64];
+        tmem_chunk(tmem, q, c, nkb > 0, v);
+        const int col0 = n0 + c * 64;
+        if (col0 < N) epi.template run_io<4>(io, slot, col0, v);
+      }
+      ptx::bulk_wait_read0();
+    } else {
+      epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
+#pragma unroll 1
+      for (int c = grp; c < BN / 64; c += 2) {
+        float v[64];
+        tmem_chunk(tmem, q, c, nkb > 0, v);
+        const int col0 = n0 + c * 64;
+        if (row < M && col0 < N) epi.template run<4>(row, col0, v);
+      }
     }
   }
   ptx::tc_fence_before();
@@ -354,13 +388,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   } else {
     const int q = warp & 3, grp = (warp - 2) >> 2;
     const int row = m0 + q * 32 + lane;
-    epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
+    if constexpr (HasAsyncIO<Epi>::value) {
+      const EpiIO io = L.io(warp - 2, m0 + q * 32, M, lane);
+      epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
+      for (int c = grp, slot = 0; c < BN / 64; c += 2, ++slot)
+        if (n0 + c * 64 < N) epi.io_issue(io, slot, n0 + c * 64);
+      ptx::mbar_arrive(io.bar);
 #pragma unroll 1
-    for (int c = grp; c < BN / 64; c += 2) {
-      float v[64];
-      tmem_chunk(tmem, q, c, nkb > 0, v);
-      const int col0 = n0 + c * 64;
-      if (row < M && col0 < N) epi.template run<4>(row, col0, v);
+      for (int c = grp, slot = 0; c < BN / 64; c += 2, ++slot) {
+        float v[64];
+        tmem_chunk(tmem, q, c, nkb > 0, v);
+        const int col0 = n0 + c * 64;
+        if (col0 < N) epi.template run_io<4>(io, slot, col0, v);
+      }
+      ptx::bulk_wait_read0();
+    } else {
+      epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
+#pragma unroll 1
+      for (int c = grp; c < BN / 64; c += 2) {
+        float v[64];
+        tmem_chunk(tmem, q, c, nkb > 0, v);
+        const int col0 = n0 + c * 64;
+        if (row < M && col0 < N) epi.template run<4>(row, col0, v);
+      }
     }
   }
   ptx::tc_fence_before();
@@ -427,6 +477,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3, grp = (warp - 2) >> 2;
     const int rl = q * 32 + lane;
     epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
+    if constexpr (HasAsyncIO<Epi>::value && !kUseTile) {
+      // the reduction phase's rows/columns of this thread (tid mapping below); loads land in the
+      // idle stages while the partials are exchanged
+      const int tid = threadIdx.x - 64, hh = tid >> 7;
+      const EpiIO io = L.io(warp - 2, m0 + (tid & 127) - lane, M, lane);
+      if (HALF_ROWS || hh == 0)
+        for (int j = 0; j < WIDTH / PIECE; ++j) {
+          const int col0 = n0 + z * SLICE + (HALF_ROWS ? hh * WIDTH : 0) + j * PIECE;
+          if (col0 < N) epi.io_issue(io, j, col0);
+        }
+      ptx::mbar_arrive(io.bar);
+    }
     float4* dst = reinterpret_cast<float4*>(part + (long)z * 128 * BN) + rl;
 #pragma unroll 1
     for (int c = grp; c < BN / 64; c += 2) {
@@ -464,7 +526,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
         const int col0 = n0 + cl;
-        if constexpr (kUseTile) {
+        if constexpr (HasAsyncIO<Epi>::value && !kUseTile) {
+          if (col0 < N) epi.template run_io<NG>(L.io(warp - 2, m0 + rl - lane, M, lane), j, col0, v);
+        } else if constexpr (kUseTile) {
           float4* d = reinterpret_cast<float4*>(stageT + rl * (SLICE + 4) + (cl - z * SLICE));
 #pragma unroll
           for (int i = 0; i < PIECE / 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
@@ -473,6 +537,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
     }
+    if constexpr (HasAsyncIO<Epi>::value && !kUseTile) ptx::bulk_wait_read0();
     if (tracing && threadIdx.x == 64) tr_ts[6] = ptx::globaltimer();
     if constexpr (kUseTile) {
       asm volatile("bar.sync 1, 256;" ::: "memory");

@@ -25,6 +25,7 @@ using namespace mlstm;
 namespace mlstm {  // trace tags of the fused epilogues (mlstm_trace_read)
 template <typename S> struct EpiTag<EpiF1<S>> { static constexpr int value = 1; };
 template <typename S> struct EpiTag<EpiF2<S>> { static constexpr int value = 2; };
+template <typename S> struct EpiTag<EpiF2IO<S>> { static constexpr int value = 2; };
 template <typename S> struct EpiTag<EpiB1<S>> { static constexpr int value = 3; };
 template <typename S> struct EpiTag<EpiB2<S>> { static constexpr int value = 4; };
 template <typename S> struct EpiTag<EpiY<S>> { static constexpr int value = 5; };
@@ -99,7 +100,8 @@ struct mlstm_ctx {
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_wh = nullptr, ev_wmh = nullptr, ev_a_end = nullptr, ev_comm = nullptr;
   bool ar_overlap = true;
-  int force_plan = 0;  // MLSTM_FORCE_PLAN (test instrument), applied while this ctx enqueues
+  int force_plan = 0;
+  int async_epi = 2;  // recurrent epilogue row I/O: 0 per-thread LSU, 1 bulk copies, 2 staged + coalesced (MLSTM_ASYNC_EPI)  // MLSTM_FORCE_PLAN (test instrument), applied while this ctx enqueues
   bool overlap_now() const { return world > 1 && ar_overlap && nmb == 1; }
   cudaGraphExec_t gA = nullptr, gB = nullptr;
   std::map<std::tuple<const void*, long, long, long, long, long, int>, CUtensorMap> maps;
@@ -321,6 +323,7 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   if (const char* v = getenv("MLSTM_PF_STASH")) c->pf_stash = v[0] != '0';
   if (const char* v = getenv("MLSTM_L2_WH")) c->l2_wh = (float)atof(v);
   if (const char* v = getenv("MLSTM_AR_OVERLAP")) c->ar_overlap = v[0] != '0';
+  if (const char* v = getenv("MLSTM_ASYNC_EPI")) c->async_epi = atoi(v);
   {
     const char* v = getenv("MLSTM_FORCE_PLAN");
     const std::string fp = v ? v : "";
@@ -610,7 +613,10 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   for (int t = 0; t < T; ++t) {
     RET_IF(gemm<S>(c, Hprev, t, Wmh, 0, B, h, h, p1, EpiF1<S>{n, t}, pf1));
     seg2.az2 = t;
-    RET_IF(gemm<S>(c, Msc, 0, Wh, 0, B, 4 * h, h, p2, EpiF2<S>{n, t, n.OHR != nullptr}, Prefetch{}, seg2));
+    if (n.OHR && c->async_epi)  // tcgen05 path (W_x x + b folded): async row I/O epilogue
+      RET_IF(gemm<S>(c, Msc, 0, Wh, 0, B, 4 * h, h, p2, EpiF2IO<S>{{n, t, 1}, c->async_epi}, Prefetch{}, seg2));
+    else
+      RET_IF(gemm<S>(c, Msc, 0, Wh, 0, B, 4 * h, h, p2, EpiF2<S>{n, t, n.OHR != nullptr}, Prefetch{}, seg2));
   }
   phase(c, PH_DEC);
   {

@@ -11,8 +11,24 @@
 #pragma once
 #include <cuda_fp16.h>
 #include <stdint.h>
+#include "ptx.cuh"
 
 namespace mlstm {
+
+// Async row I/O for epilogues that declare kAsyncIO: after the main loop the pipeline stages are
+// idle, so each epilogue warp gets a private staging window there (kWarpStage bytes) plus an
+// mbarrier for its loads.  Inputs come in by per-row bulk copies (issued before the accumulator is
+// read, so their latency overlaps the TMEM loads / split-K reduction); outputs are written to the
+// window and leave by per-row bulk copies -- no 32-line LSU wavefronts per warp instruction.
+constexpr int kWarpStageBytes = 24 * 1024;
+struct EpiIO {
+  uint8_t* buf;   // this warp's staging window (16-byte aligned)
+  uint64_t* bar;  // this warp's load barrier (count 32: every lane arrives once per launch)
+  int row0;       // accumulator row of lane 0
+  int nvalid;     // rows of this warp inside M: lane < nvalid
+  int lane;
+  __device__ __forceinline__ bool valid() const { return lane < nvalid; }
+};
 
 __host__ __device__ __forceinline__ int int_row(int g, int j) { return (j >> 4) * 64 + g * 16 + (j & 15); }
 __host__ __device__ __forceinline__ int canon_of_int(int r, int h) {
