@@ -43,9 +43,8 @@ struct EpiF1 {
   template <int NG>
   __device__ __forceinline__ void run(int b, int col0, const float* v) const {
     const float* mx = n.tab + (long)n.byte_at(b, t) * 5 * n.h + col0;
-    S* mrow = n.Mscr + (long)b * n.h + col0;
+    S* mrow = n.Mrm + ((long)t * n.B + b) * n.h + col0;
     S* arow = n.Astash + ((long)t * n.B + b) * n.h + col0;
-    const long kc = n.kcol(t, b);
 #pragma unroll
     for (int q = 0; q < NG; ++q) {
       float x[16], m[16];
@@ -54,8 +53,6 @@ struct EpiF1 {
       for (int i = 0; i < 16; ++i) m[i] = x[i] * v[16 * q + i];
       st16(mrow + 16 * q, m);
       st16(arow + 16 * q, v + 16 * q);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) n.MT[(long)(col0 + 16 * q + i) * n.ldK + kc] = to_s<S>(m[i]);
     }
   }
 };
@@ -107,9 +104,6 @@ struct EpiF2 {  // one call = 4 gates x 16 units: NG must be 4
     st16(grow + 48, gu);
     st16(n.Hrm + ((long)(t + 1) * n.B + b) * h + j0, hv);
     st16(n.Crm + ((long)(t + 1) * n.B + b) * h + j0, cv);
-    const long kc = n.kcol(t + 1, b);
-#pragma unroll
-    for (int jj = 0; jj < 16; ++jj) n.HT[(long)(j0 + jj) * n.ldH + kc] = to_s<S>(hv[jj]);
   }
 };
 
@@ -199,11 +193,6 @@ struct EpiF2IO : EpiF2<S> {
       warp_rows_out(reinterpret_cast<uint8_t*>(n.Hrm + ((long)(t + 1) * n.B + b0) * h + j0), 2L * h, sb + kH, 48, 32,
                     io.nvalid, lane);
     }
-    if (io.valid()) {
-      const long kc = n.kcol(t + 1, b);
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj) n.HT[(long)(j0 + jj) * n.ldH + kc] = hv[jj];
-    }
   }
 };
 
@@ -268,20 +257,11 @@ __device__ __forceinline__ void gate_bwd16(const Net<S>& n, int s, int b, int j0
     dcnew[jj] = dc * f;
   }
   st16(n.dC + (long)b * h + j0, dcnew);
-  S* zrow = n.dZscr + (long)b * 4 * h + (long)(j0 >> 4) * 64;
+  S* zrow = n.G5 + ((long)s * n.B + b) * 5 * h + h + (long)(j0 >> 4) * 64;
   st16(zrow, dzi);
   st16(zrow + 16, dzf);
   st16(zrow + 32, dzo);
   st16(zrow + 48, dzu);
-  const long kc = n.kcol(s, b);
-  const long r0 = (long)h + (long)(j0 >> 4) * 64;
-#pragma unroll
-  for (int jj = 0; jj < 16; ++jj) {
-    n.dGT[(r0 + jj) * n.ldK + kc] = to_s<S>(dzi[jj]);
-    n.dGT[(r0 + 16 + jj) * n.ldK + kc] = to_s<S>(dzf[jj]);
-    n.dGT[(r0 + 32 + jj) * n.ldK + kc] = to_s<S>(dzo[jj]);
-    n.dGT[(r0 + 48 + jj) * n.ldK + kc] = to_s<S>(dzu[jj]);
-  }
 }
 
 // (c-1) backward GEMM 1, dM_t = dZ_t W_h:  dA = dM * mx,  dMX = dM * a.
@@ -295,8 +275,8 @@ struct EpiB1 {
   __device__ __forceinline__ void run(int b, int col0, const float* v) const {
     const float* mx = n.tab + (long)n.byte_at(b, t) * 5 * n.h + col0;
     const S* arow = n.Astash + ((long)t * n.B + b) * n.h + col0;
-    S* darow = n.dAscr + (long)b * n.h + col0;
-    const long kc = n.kcol(t, b);
+    S* darow = n.dA + ((long)t * n.B + b) * n.h + col0;
+    S* mxrow = n.G5 + ((long)t * n.B + b) * 5 * n.h + col0;  // dMX block of the stash row
 #pragma unroll
     for (int q = 0; q < NG; ++q) {
       float x[16], a[16], da[16], dmx[16];
@@ -308,12 +288,7 @@ struct EpiB1 {
         dmx[i] = v[16 * q + i] * a[i];
       }
       st16(darow + 16 * q, da);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const long r = col0 + 16 * q + i;
-        n.dAT[r * n.ldK + kc] = to_s<S>(da[i]);
-        n.dGT[r * n.ldK + kc] = to_s<S>(dmx[i]);
-      }
+      st16(mxrow + 16 * q, dmx);
     }
   }
 };
@@ -323,9 +298,8 @@ struct EpiB1 {
 // T[rows][U] (row stride ldt, columns = hidden units n0..n0+U) sits in shared memory).  The row-
 // per-thread form touches 32 cache lines per warp instruction, which makes the L1 wavefront rate,
 // not DRAM, the bound; here 16 lanes x 4 units cover 64 units of one row (two rows per warp
-// instruction, 8/16-byte vectors) and each thread batches RB rows' loads before any store.  The
-// transposed dZ stash goes through shared memory Zs[gate*U + unit][row] and leaves with lanes
-// along rows (8-byte stores of 4 consecutive batch rows).  256 threads, tid in [0, 256).
+// instruction, 8/16-byte vectors) and each thread batches RB rows' loads before any store.
+// 256 threads, tid in [0, 256).
 __device__ __forceinline__ void epi_bar256() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 template <typename S>
@@ -336,10 +310,6 @@ __device__ __forceinline__ void b2_tile(const Net<S>& n, int s, const float* T, 
   const int ug = tid % ng, rr = tid / ng;
   const int u0 = 4 * ug, j = n0 + u0;
   const long gcol = (long)(j >> 4) * 64 + (j & 15);  // internal column of gate i of unit j
-  // Zs[row][gate * U + unit], row stride 4U + 2 elements: pass-1 writes are contiguous vectors,
-  // pass-2 reads (lanes on consecutive rows) hit distinct banks.
-  const int ldz = 4 * U + 2;
-  S* Zs = reinterpret_cast<S*>(sm);
   if (rr < rpi) {
     for (int rb = rr; rb < rows; rb += rpi * RB) {
       float4 dh[RB], gi[RB], gf[RB], go[RB], gu[RB], c[RB], cp[RB], dcn[RB];
@@ -380,30 +350,13 @@ __device__ __forceinline__ void b2_tile(const Net<S>& n, int s, const float* T, 
         }
         const long b = m0 + r;
         st4(n.dC + b * h + j, make_float4(dcw[0], dcw[1], dcw[2], dcw[3]));
-        S* zr = n.dZscr + b * 4 * h + gcol;
+        S* zr = n.G5 + ((long)s * n.B + b) * 5 * h + h + gcol;
         st4(zr, make_float4(dzi[0], dzi[1], dzi[2], dzi[3]));
         st4(zr + 16, make_float4(dzf[0], dzf[1], dzf[2], dzf[3]));
         st4(zr + 32, make_float4(dzo[0], dzo[1], dzo[2], dzo[3]));
         st4(zr + 48, make_float4(dzu[0], dzu[1], dzu[2], dzu[3]));
-        S* zs = Zs + r * ldz + u0;
-        st4s(zs, make_float4(dzi[0], dzi[1], dzi[2], dzi[3]));
-        st4s(zs + U, make_float4(dzf[0], dzf[1], dzf[2], dzf[3]));
-        st4s(zs + 2 * U, make_float4(dzo[0], dzo[1], dzo[2], dzo[3]));
-        st4s(zs + 3 * U, make_float4(dzu[0], dzu[1], dzu[2], dzu[3]));
       }
     }
-  }
-  epi_bar256();
-  // pass 2: dGT[h + gate-unit row][kcol(s, b)]: lanes on consecutive batch rows (2-byte stores,
-  // 64 contiguous bytes per warp instruction)
-  const int warp = tid >> 5, lane = tid & 31;
-  const long kc0 = n.kcol(s, m0);
-  for (int g_u = warp; g_u < 4 * U; g_u += 8) {
-    const int g = g_u / U, u = g_u - g * U;
-    S* dst = n.dGT + ((long)h + int_row(g, n0 + u)) * n.ldK + kc0;
-#pragma unroll
-    for (int r = lane; r < 128; r += 32)
-      if (r < rows) dst[r] = Zs[r * ldz + g_u];
   }
 }
 

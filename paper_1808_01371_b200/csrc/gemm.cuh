@@ -24,6 +24,7 @@ namespace mlstm {
 constexpr int kEpiWarps = 8;
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
 constexpr int kGemmStaticB = 1;  // B operand is a weight untouched by the preceding kernels
+constexpr int kGemmRasterM = 2;  // launch order M-fastest (CTAs running together share a B tile)
 
 // ---- optional intra-kernel timeline (mlstm_trace_enable): one record per CTA,
 // {tag, cta, t_start, t_first_tma, t_first_full, t_acc_ready, t_reduced, t_end} in ns.
@@ -154,7 +155,9 @@ struct Seg2 {
   int az2, bz2;
 };
 
-template <class C, bool PAIR>
+// MN: both operands MN-major ([K][M] / [K][N] in memory, the weight-gradient GEMMs D = A^T B over
+// a long K = T*B): each stage is one 64-row K block loaded as 64-wide MN boxes.
+template <class C, bool PAIR, bool MN = false>
 __device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUtensorMap* tmA, const CUtensorMap* tmB,
                                              const CUtensorMap* tmA2, const CUtensorMap* tmB2, Seg2 sg, int nkb,
                                              int kb0, int m0, int nb0, int az, int bz, uint32_t polA,
@@ -163,6 +166,15 @@ __device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUten
   const uint64_t pa = ptx::make_policy(polA), pb = ptx::make_policy(polB);
   const uint32_t tx = PAIR ? 2 * C::STAGE_BYTES : C::STAGE_BYTES;
   auto loadA = [&](int s, int kb) {
+    if constexpr (MN) {
+#pragma unroll
+      for (int i = 0; i < C::BM / 64; ++i) {
+        uint8_t* dst = L.sA + s * C::A_BYTES + i * 8192;
+        if (PAIR) ptx::tma_load_3d_2sm(dst, tmA, bar_leader0 + s * 8, m0 + 64 * i, kb * C::BK, az, pa);
+        else ptx::tma_load_3d(dst, tmA, &L.full[s], m0 + 64 * i, kb * C::BK, az, pa);
+      }
+      return;
+    }
     const bool s2 = kb >= sg.kb_seg0;
     const CUtensorMap* m = s2 ? tmA2 : tmA;
     const int k = (s2 ? kb - sg.kb_seg0 : kb) * C::BK, z = s2 ? sg.az2 : az;
@@ -170,6 +182,16 @@ __device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUten
     else ptx::tma_load_3d(L.sA + s * C::A_BYTES, m, &L.full[s], k, m0, z, pa);
   };
   auto loadB = [&](int s, int kb) {
+    if constexpr (MN) {
+#pragma unroll
+      static_assert(!MN || C::B_BYTES % 8192 == 0, "MN-major B needs 64-wide boxes per CTA");
+      for (int i = 0; i < C::B_BYTES / 8192; ++i) {
+        uint8_t* dst = L.sB + s * C::B_BYTES + i * 8192;
+        if (PAIR) ptx::tma_load_3d_2sm(dst, tmB, bar_leader0 + s * 8, nb0 + 64 * i, kb * C::BK, bz, pb);
+        else ptx::tma_load_3d(dst, tmB, &L.full[s], nb0 + 64 * i, kb * C::BK, bz, pb);
+      }
+      return;
+    }
     const bool s2 = kb >= sg.kb_seg0;
     const CUtensorMap* m = s2 ? tmB2 : tmB;
     const int k = (s2 ? kb - sg.kb_seg0 : kb) * C::BK, z = s2 ? sg.bz2 : bz;
@@ -197,10 +219,11 @@ __device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUten
 
 // MMA issuer (one thread of the leader CTA): BK/16 tcgen05.mma per stage, commit frees the stage;
 // the final commit signals the accumulator.  PAIR: M = 256 over the CTA pair, commits multicast.
-template <class C, bool PAIR, int MMA_N>
+template <class C, bool PAIR, int MMA_N, bool MN = false>
 __device__ __forceinline__ void gemm_mma(const SmemLayout<C>& L, uint32_t tmem, int nkb, uint16_t pair_mask,
                                          uint64_t* trace_slot) {
-  constexpr uint32_t idesc = ptx::idesc_f16_f32(PAIR ? 256 : 128, MMA_N);
+  constexpr uint32_t idesc = ptx::idesc_f16_f32(PAIR ? 256 : 128, MMA_N, MN);
+  constexpr int kstep = MN ? 2048 >> 4 : 32 >> 4;  // descriptor start-address step per K = 16
 #pragma unroll 1
   for (int i = 0; i < nkb; ++i) {
     const int s = i % C::STAGES;
@@ -208,12 +231,13 @@ __device__ __forceinline__ void gemm_mma(const SmemLayout<C>& L, uint32_t tmem, 
     ptx::mbar_wait(&L.full[s], ph);
     ptx::tc_fence_after();
     if (trace_slot && i == 0) *trace_slot = ptx::globaltimer();
-    const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(L.sA + s * C::A_BYTES));
-    const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(L.sB + s * C::B_BYTES));
+    const uint32_t sa = ptx::smem_u32(L.sA + s * C::A_BYTES), sb = ptx::smem_u32(L.sB + s * C::B_BYTES);
+    const uint64_t ad = MN ? ptx::sdesc_mnmajor_sw128(sa) : ptx::sdesc_kmajor_sw128(sa);
+    const uint64_t bd = MN ? ptx::sdesc_mnmajor_sw128(sb) : ptx::sdesc_kmajor_sw128(sb);
 #pragma unroll
     for (int k = 0; k < C::BK / 16; ++k) {
-      if (PAIR) ptx::mma_f16_2sm(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
-      else ptx::mma_f16(tmem, ad + 2 * k, bd + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
+      if (PAIR) ptx::mma_f16_2sm(tmem, ad + kstep * k, bd + kstep * k, idesc, (i | k) != 0 ? 1u : 0u);
+      else ptx::mma_f16(tmem, ad + kstep * k, bd + kstep * k, idesc, (i | k) != 0 ? 1u : 0u);
     }
     if (PAIR) ptx::mma_commit_2sm_mc(&L.empty[s], pair_mask);
     else ptx::mma_commit(&L.empty[s]);
@@ -234,6 +258,40 @@ __device__ __forceinline__ void tmem_chunk(uint32_t tmem, int q, int c, bool hav
   } else {
 #pragma unroll
     for (int i = 0; i < 64; ++i) v[i] = 0.f;
+  }
+}
+
+// Tile epilogue on a one-tile-per-CTA engine: the 128 x BN accumulator goes through shared memory
+// in 64-column slices (stageT[128][68] fp32 in the idle stages, then epi.tile() with its scratch
+// behind it), so tile epilogues (coalesced, batched) also run on the CTA-pair / 1-CTA plans that
+// large batches select.  Epilogue warps only (256 threads, named barrier 1).
+template <int BN, class Epi, class C>
+__device__ __forceinline__ void tile_epilogue(const SmemLayout<C>& L, uint32_t tmem, bool have, int m0, int n0, int M,
+                                              int N, const Epi& epi) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, grp = (warp - 2) >> 2, tid = threadIdx.x - 64;
+  float* stageT = reinterpret_cast<float*>(L.sA);
+  uint8_t* scratch = reinterpret_cast<uint8_t*>(stageT + 128 * 68);
+  const int rows = min(128, M - m0);
+#pragma unroll 1
+  for (int c = 0; c < BN / 64; ++c) {
+    float v[32];
+    if (have) {
+      const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + c * 64 + grp * 32;
+      ptx::tmem_ld16(ta, v);
+      ptx::tmem_ld16(ta + 16, v + 16);
+      ptx::tmem_ld_wait();
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    }
+    float4* d = reinterpret_cast<float4*>(stageT + (q * 32 + lane) * 68 + grp * 32);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const int c0 = n0 + c * 64;
+    if (rows > 0 && c0 < N) epi.tile(stageT, 68, m0, c0, min(64, N - c0), rows, scratch, tid);
+    asm volatile("bar.sync 1, 256;" ::: "memory");
   }
 }
 
@@ -286,7 +344,7 @@ __device__ __forceinline__ void epi_begin(uint64_t* accf, bool have, uint64_t* t
   }
 
 // ---------------------------------------------------------------------------------------------
-template <int BN, class Epi>
+template <int BN, class Epi, bool MN = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, Seg2 sg, int M,
@@ -297,7 +355,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const SmemLayout<C> L(smem_raw);
   MLSTM_TRACE_BEGIN();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * C::BM, n0 = blockIdx.x * BN;
+  // kGemmRasterM: M-fastest raster -- CTAs launched together share their B (weight) tile, so a
+  // multi-wave per-timestep GEMM streams each weight tile from HBM once (its A operand is small and
+  // L2-resident).  Otherwise N-fastest (weight gradients: both operands stream along a long K).
+  const int lin = blockIdx.x + gridDim.x * blockIdx.y;
+  const bool rm = flags & kGemmRasterM;
+  const int m0 = (rm ? lin % gridDim.y : blockIdx.y) * C::BM, n0 = (rm ? lin / gridDim.y : blockIdx.x) * BN;
   const int total_kb = (K + C::BK - 1) / C::BK;
   const int kb0 = blockIdx.z * kb_per_split;
   const int nkb = max(0, min(kb_per_split, total_kb - kb0));
@@ -309,16 +372,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       if (nkb > 0)
-        gemm_produce<C, false>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true, 0,
-                               MLSTM_TRACE_SLOT(1));
+        gemm_produce<C, false, MN>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true,
+                                   0, MLSTM_TRACE_SLOT(1));
       l2_prefetch(pj);
     }
   } else if (warp == 1) {
-    if (lane == 0 && nkb > 0) gemm_mma<C, false, BN>(L, tmem, nkb, 0, MLSTM_TRACE_SLOT(2));
+    if (lane == 0 && nkb > 0) gemm_mma<C, false, BN, MN>(L, tmem, nkb, 0, MLSTM_TRACE_SLOT(2));
   } else {
     const int q = warp & 3, grp = (warp - 2) >> 2;
     const int row = m0 + q * 32 + lane;
-    if constexpr (HasAsyncIO<Epi>::value) {
+    if constexpr (HasTile<Epi>::value) {
+      epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
+      tile_epilogue<BN>(L, tmem, nkb > 0, m0, n0, M, N, epi);
+    } else if constexpr (HasAsyncIO<Epi>::value) {
       const EpiIO io = L.io(warp - 2, m0 + q * 32, M, lane);
       epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
       for (int c = grp, slot = 0; c < BN / 64; c += 2, ++slot)
@@ -353,7 +419,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 // ---------------------------------------------------------------------------------------------
-template <int BN, class Epi>
+template <int BN, class Epi, bool MN = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, Seg2 sg, int M,
@@ -366,8 +432,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
   const bool leader = rank == 0;
-  const int n0 = (blockIdx.x >> 1) * BN;
-  const int m0 = blockIdx.y * 256 + rank * 128;
+  const int lin = (blockIdx.x >> 1) + (gridDim.x >> 1) * blockIdx.y;  // raster: see gemm_tc_kernel
+  const bool rm = flags & kGemmRasterM;
+  const int n0 = (rm ? lin / gridDim.y : (blockIdx.x >> 1)) * BN;
+  const int m0 = (rm ? lin % gridDim.y : blockIdx.y) * 256 + rank * 128;
   const int total_kb = (K + C::BK - 1) / C::BK;
   const int kb0 = blockIdx.z * kb_per_split;
   const int nkb = max(0, min(kb_per_split, total_kb - kb0));
@@ -379,16 +447,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       if (nkb > 0)
-        gemm_produce<C, true>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0 + rank * (BN / 2), az, bz, polA, polB, flags,
+        gemm_produce<C, true, MN>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0 + rank * (BN / 2), az, bz, polA, polB, flags,
                               leader, ptx::mapa_shared(ptx::smem_u32(&L.full[0]), 0), MLSTM_TRACE_SLOT(1));
       l2_prefetch(pj);
     }
   } else if (warp == 1) {
-    if (leader && lane == 0 && nkb > 0) gemm_mma<C, true, BN>(L, tmem, nkb, 0x3, MLSTM_TRACE_SLOT(2));
+    if (leader && lane == 0 && nkb > 0) gemm_mma<C, true, BN, MN>(L, tmem, nkb, 0x3, MLSTM_TRACE_SLOT(2));
   } else {
     const int q = warp & 3, grp = (warp - 2) >> 2;
     const int row = m0 + q * 32 + lane;
-    if constexpr (HasAsyncIO<Epi>::value) {
+    if constexpr (HasTile<Epi>::value) {
+      epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
+      tile_epilogue<BN>(L, tmem, nkb > 0, m0, n0, M, N, epi);
+    } else if constexpr (HasAsyncIO<Epi>::value) {
       const EpiIO io = L.io(warp - 2, m0 + q * 32, M, lane);
       epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
       for (int c = grp, slot = 0; c < BN / 64; c += 2, ++slot)
@@ -429,7 +500,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 // columns [z*256/S, (z+1)*256/S) of its 128 rows over the S partials in fixed order z' = 0..S-1
 // (deterministic) and runs the fused epilogue on that slice -- the 256 epilogue threads each take
 // half a row of the slice, or a whole row when the epilogue needs full 64-column chunks.
-template <int S, class Epi>
+template <int S, class Epi, bool MN = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc1s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, Seg2 sg, int M,
@@ -467,12 +538,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       if (nkb > 0)
-        gemm_produce<C, false>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true, 0,
-                               MLSTM_TRACE_SLOT(1));
+        gemm_produce<C, false, MN>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true,
+                                   0, MLSTM_TRACE_SLOT(1));
       l2_prefetch(pj);
     }
   } else if (warp == 1) {
-    if (lane == 0 && nkb > 0) gemm_mma<C, false, BN>(L, tmem, nkb, 0, MLSTM_TRACE_SLOT(2));
+    if (lane == 0 && nkb > 0) gemm_mma<C, false, BN, MN>(L, tmem, nkb, 0, MLSTM_TRACE_SLOT(2));
   } else {
     const int q = warp & 3, grp = (warp - 2) >> 2;
     const int rl = q * 32 + lane;
@@ -573,7 +644,7 @@ __device__ __forceinline__ float ld_as_float<__half>(const __half* p) {
 template <typename T, class Epi>
 __global__ void __launch_bounds__(128)
     gemm_simt_kernel(const T* __restrict__ A, long lda, const T* __restrict__ B, long ldb, int M, int N, int K,
-                     int k_per_split, Epi epi) {
+                     int k_per_split, int mn, Epi epi) {
   __shared__ float As[32][129];
   __shared__ __align__(16) float Bs[32][64];
   const int tid = threadIdx.x;
@@ -587,13 +658,14 @@ __global__ void __launch_bounds__(128)
   for (int kk = kbeg; kk < kend; kk += 32) {
 #pragma unroll 4
     for (int i = tid; i < 128 * 32; i += 128) {
-      const int r = i >> 5, k = i & 31, gr = m0 + r, gk = kk + k;
-      As[k][r] = (gr < M && gk < kend) ? ld_as_float(A + (long)gr * lda + gk) : 0.f;
+      // mn: operands MN-major (element (r, k) at k * ld + r), lanes along r
+      const int r = mn ? (i & 127) : (i >> 5), k = mn ? (i >> 7) : (i & 31), gr = m0 + r, gk = kk + k;
+      As[k][r] = (gr < M && gk < kend) ? ld_as_float(A + (mn ? (long)gk * lda + gr : (long)gr * lda + gk)) : 0.f;
     }
 #pragma unroll 4
     for (int i = tid; i < 64 * 32; i += 128) {
-      const int n = i >> 5, k = i & 31, gn = n0 + n, gk = kk + k;
-      Bs[k][n] = (gn < N && gk < kend) ? ld_as_float(B + (long)gn * ldb + gk) : 0.f;
+      const int n = mn ? (i & 63) : (i >> 5), k = mn ? (i >> 6) : (i & 31), gn = n0 + n, gk = kk + k;
+      Bs[k][n] = (gn < N && gk < kend) ? ld_as_float(B + (mn ? (long)gk * ldb + gn : (long)gn * ldb + gk)) : 0.f;
     }
     __syncthreads();
 #pragma unroll 2

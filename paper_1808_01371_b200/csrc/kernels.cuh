@@ -97,7 +97,6 @@ __global__ void state_in_kernel(Net<S> n, int slot) {
     const S hv = rst ? to_s<S>(0.f) : n.hstate[so + i];
     const float cv = rst ? 0.f : n.cstate[so + i];
     n.Hrm[i] = hv;
-    n.HT[(long)j * n.ldH + b] = hv;
     n.Crm[i] = cv;
   }
 }
@@ -129,21 +128,17 @@ __global__ void grad_accum_kernel(Net<S> n) {
   }
 }
 
-// One-hot of the input bytes, transposed: OHT[v][t*Bp+b] = [bytes[b][t] == v] (exact in fp16).
+// One-hot of the input bytes, row-major: OHR[t][b][v] = [bytes[b][t] == v] (exact in fp16).
 template <typename S>
 __global__ void onehot_kernel(Net<S> n) {
   const long TB = (long)n.T * n.B;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < TB; i += (long)gridDim.x * blockDim.x) {
     const int t = (int)(i / n.B), b = (int)(i % n.B);
     const int v0 = n.byte_at(b, t);
-    const long kc = n.kcol(t, b);
-    for (int v = 0; v < 256; ++v) n.OHT[(long)v * n.ldK + kc] = to_s<S>(v == v0 ? 1.f : 0.f);
-    if (n.OHR) {
-      S* row = n.OHR + i * 256;
-      for (int v = 0; v < 256; v += 4)
-        st4(row + v, make_float4(v == v0 ? 1.f : 0.f, v + 1 == v0 ? 1.f : 0.f, v + 2 == v0 ? 1.f : 0.f,
-                                 v + 3 == v0 ? 1.f : 0.f));
-    }
+    S* row = n.OHR + i * 256;
+    for (int v = 0; v < 256; v += 4)
+      st4(row + v, make_float4(v == v0 ? 1.f : 0.f, v + 1 == v0 ? 1.f : 0.f, v + 2 == v0 ? 1.f : 0.f,
+                               v + 3 == v0 ? 1.f : 0.f));
   }
 }
 
@@ -234,15 +229,6 @@ __global__ void __launch_bounds__(256) ce_kernel(Net<S> n, int Be, float inv_den
       float s = 0.f;
       for (int i = 0; i < 32; ++i) s += tile[i][v];
       n.colsum_part[(long)blockIdx.x * 256 + v] = s;
-    }
-    const long r = r0 + lane;
-    if (r < R) {
-      const long kc = n.kcol((int)(r / n.B), (int)(r % n.B));
-#pragma unroll 4
-      for (int vv = 0; vv < 32; ++vv) {
-        const int v = warp * 32 + vv;
-        n.dYT[(long)v * n.ldK + kc] = to_s<S>(tile[lane][v]);
-      }
     }
   }
 }

@@ -33,6 +33,10 @@ template <typename S> struct EpiTag<EpiDHdec<S>> { static constexpr int value = 
 template <typename S> struct EpiTag<EpiTab<S>> { static constexpr int value = 7; };
 template <typename S> struct EpiTag<EpiWgrad<S>> { static constexpr int value = 8; };
 template <> struct EpiTag<EpiPartial> { static constexpr int value = 9; };
+// epilogues that run on MN-major operands (the weight-gradient GEMMs)
+template <class E> constexpr bool kMNEpi = false;
+template <typename S> constexpr bool kMNEpi<EpiWgrad<S>> = true;
+template <> constexpr bool kMNEpi<EpiPartial> = true;
 }  // namespace mlstm
 
 namespace {
@@ -48,6 +52,7 @@ struct Opd {  // K-major operand view: [zdim][rows][K], element strides ld (row)
   long rows, K, ld, zdim, zstride;
   uint32_t pol = 0;     // L2 policy code for its TMA loads (ptx::make_policy)
   bool weight = false;  // a parameter copy: not written by any kernel of the step before the optimiser
+  bool mn = false;      // MN-major instead: element (r, k) at z*zstride + k*ld + r  ([K][rows] in memory)
 };
 constexpr uint32_t kPolFirst = 1u << 8;
 inline uint32_t pol_last(float frac) { return (2u << 8) | (uint32_t)(frac * 255.f + 0.5f); }
@@ -72,7 +77,7 @@ struct mlstm_ctx {
   bool mixed = true, tc = true;
   int h = 0, e = 0, B = 0, T = 0, Bp = 0;  // B = rows per micro-batch
   int Bfull = 0, nmb = 1;                    // rows per rank, micro-batches per step
-  long ldK = 0, ldH = 0, P = 0, Kt = 0;
+  long P = 0, Kt = 0;
   ParamOffsets po{};
   uint8_t* ws = nullptr;
   size_t ws_bytes = 0;
@@ -217,7 +222,7 @@ void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
   const long P = c->P;
   n.h = h; n.e = e; n.B = B; n.T = T; n.Bp = c->Bp;
   n.Bfull = c->Bfull; n.nmb = c->nmb;
-  n.ldK = c->ldK; n.ldH = c->ldH; n.po = c->po;
+  n.po = c->po;
   n.master = cv.take<float>(P);
   c->adam_m = cv.take<float>(P);
   c->adam_v = cv.take<float>(P);
@@ -236,26 +241,20 @@ void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
   n.reset = c->reset;
   n.tab = cv.take<float>(256L * 5 * h);
   n.XZT = c->tc ? cv.take<S>(4L * h * 256) : nullptr;
-  n.OHR = c->tc ? cv.take<S>((long)T * B * 256) : nullptr;
+  n.OHR = cv.take<S>((long)T * B * 256);
   n.Hrm = cv.take<S>((long)(T + 1) * B * h);
-  n.HT = cv.take<S>((long)h * c->ldH);
   n.Crm = cv.take<float>((long)(T + 1) * B * h);
-  n.Mscr = cv.take<S>((long)B * h);
-  n.MT = cv.take<S>((long)h * c->ldK);
+  n.Mrm = cv.take<S>((long)T * B * h);
   n.Astash = cv.take<S>((long)T * B * h);
   n.Gates = cv.take<S>((long)T * B * 4 * h);
   n.Y = cv.take<float>((long)T * B * 256);
   n.lossrow = cv.take<float>((long)T * B);
   n.dY = cv.take<S>((long)T * B * 256);
-  n.dYT = cv.take<S>(256L * c->ldK);
-  n.OHT = cv.take<S>(256L * c->ldK);
   // tcgen05 path: dH_dec,t = dY_t W_dec enters the B2 accumulator as a second K segment (no buffer)
   n.dHdec = c->tc ? nullptr : cv.take<float>((long)T * B * h);
-  n.dZscr = cv.take<S>((long)B * 4 * h);
-  n.dAscr = cv.take<S>((long)B * h);
+  n.G5 = cv.take<S>((long)T * B * 5 * h);
+  n.dA = cv.take<S>((long)T * B * h);
   n.dC = cv.take<float>((long)B * h);
-  n.dGT = cv.take<S>(5L * h * c->ldK);
-  n.dAT = cv.take<S>((long)h * c->ldK);
   // split-K partial buffer: the largest split GEMM among the weight gradients
   long part = 64;
   const long K = c->Kt;
@@ -309,10 +308,8 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   c->B = cfg->micro_batch > 0 ? cfg->micro_batch : cfg->batch;  // rows per micro-batch
   c->nmb = c->Bfull / c->B;
   c->T = cfg->seq_len;
-  c->Bp = (int)rup(c->B, 8);
-  c->Kt = (long)c->T * c->Bp;
-  c->ldK = rup(c->Kt, 64);
-  c->ldH = rup((long)(c->T + 1) * c->Bp, 64);
+  c->Bp = c->B;
+  c->Kt = (long)c->T * c->B;  // K of the weight-gradient GEMMs: every (t, b) of the micro-batch
   c->po.set(c->h, c->e);
   c->P = c->po.P;
   c->mixed = cfg->precision == MLSTM_MIXED;
@@ -360,13 +357,14 @@ bool get_encoder() {
 }
 
 const CUtensorMap* get_map(mlstm_ctx* c, const Opd& o, int box_rows) {
+  if (o.mn) box_rows = -1;  // MN-major maps always use 64 x 64 boxes
   auto key = std::make_tuple(o.ptr, o.rows, o.K, o.ld, o.zdim, o.zstride, box_rows);
   auto it = c->maps.find(key);
   if (it != c->maps.end()) return &it->second;
   CUtensorMap m;
-  cuuint64_t dims[3] = {(cuuint64_t)o.K, (cuuint64_t)o.rows, (cuuint64_t)o.zdim};
+  cuuint64_t dims[3] = {(cuuint64_t)(o.mn ? o.rows : o.K), (cuuint64_t)(o.mn ? o.K : o.rows), (cuuint64_t)o.zdim};
   cuuint64_t strides[2] = {(cuuint64_t)o.ld * 2, (cuuint64_t)o.zstride * 2};
-  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t box[3] = {64, (cuuint32_t)(o.mn ? 64 : box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(o.ptr), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -419,17 +417,17 @@ cudaError_t launch_gemm(mlstm_ctx* c, Kern kern, dim3 grid, int smem, int cluste
   return e;
 }
 
-template <int BN, class Epi>
+template <int BN, class Epi, bool MN = false>
 cudaError_t launch_tc(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, const CUtensorMap* ma2,
                       const CUtensorMap* mb2, Seg2 sg, int M, int N, int K, int az, int bz,
                       uint32_t pa, uint32_t pb, int flags, int splits, PrefetchJob pj,
                       const Epi& epi) {
   const int kb = (K + 63) / 64, kbps = (kb + splits - 1) / splits;
-  return launch_gemm(c, gemm_tc_kernel<BN, Epi>, dim3((N + BN - 1) / BN, (M + 127) / 128, splits), TcCfg<BN>::SMEM,
+  return launch_gemm(c, gemm_tc_kernel<BN, Epi, MN>, dim3((N + BN - 1) / BN, (M + 127) / 128, splits), TcCfg<BN>::SMEM,
                      1, *ma, *mb, *ma2, *mb2, sg, M, N, K, az, bz, kbps, pa, pb, flags, pj, epi);
 }
 
-template <int S, class Epi>
+template <int S, class Epi, bool MN = false>
 cudaError_t launch_tc1s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, const CUtensorMap* ma2,
                         const CUtensorMap* mb2, Seg2 sg, int M, int N, int K, int az,
                         int bz, uint32_t pa, uint32_t pb, int flags, PrefetchJob pj,
@@ -437,18 +435,42 @@ cudaError_t launch_tc1s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* 
   const int kb = (K + 63) / 64, kbps = (kb + S - 1) / S;
   if ((long)S * ((N + 255) / 256) * ((M + 127) / 128) * 128 * 256 > kSplitScratchFloats)
     return cudaErrorInvalidConfiguration;  // the split-K partials would not fit the scratch
-  return launch_gemm(c, gemm_tc1s_kernel<S, Epi>, dim3(S * ((N + 255) / 256), (M + 127) / 128, 1), TcCfg<256>::SMEM,
+  return launch_gemm(c, gemm_tc1s_kernel<S, Epi, MN>, dim3(S * ((N + 255) / 256), (M + 127) / 128, 1), TcCfg<256>::SMEM,
                      S, *ma, *mb, *ma2, *mb2, sg, M, N, K, az, bz, kbps, pa, pb, flags, pj, c->split_scratch, epi);
 }
 
-template <int BN, class Epi>
+template <int BN, class Epi, bool MN = false>
 cudaError_t launch_tc2(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, const CUtensorMap* ma2,
                        const CUtensorMap* mb2, Seg2 sg, int M, int N, int K, int az,
                        int bz, uint32_t pa, uint32_t pb, int flags, int splits, PrefetchJob pj,
                        const Epi& epi) {
   const int kb = (K + 63) / 64, kbps = (kb + splits - 1) / splits;
-  return launch_gemm(c, gemm_tc2_kernel<BN, Epi>, dim3(2 * ((N + BN - 1) / BN), (M + 255) / 256, splits),
+  return launch_gemm(c, gemm_tc2_kernel<BN, Epi, MN>, dim3(2 * ((N + BN - 1) / BN), (M + 255) / 256, splits),
                      Tc2Cfg<BN>::SMEM, 2, *ma, *mb, *ma2, *mb2, sg, M, N, K, az, bz, kbps, pa, pb, flags, pj, epi);
+}
+
+// Engine dispatch for one plan (MN: both operands MN-major).
+template <bool MN, class Epi>
+cudaError_t dispatch_tc(mlstm_ctx* c, const Plan& p, const CUtensorMap* ma, const CUtensorMap* mb,
+                        const CUtensorMap* ma2, const CUtensorMap* mb2, Seg2 sg, int M, int N, int K, int az, int bz,
+                        uint32_t pa, uint32_t pb, int gflags, PrefetchJob pj, const Epi& epi) {
+  if (p.cluster)
+    return p.splits == 2 ? launch_tc1s<2, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, pj, epi)
+                         : launch_tc1s<4, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, pj, epi);
+  if (p.pair) {
+    if (MN || p.bn == 256)
+      return launch_tc2<256, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
+    if constexpr (!MN) {
+      if (p.bn == 128)
+        return launch_tc2<128, Epi>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
+      return launch_tc2<64, Epi>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
+    }
+  }
+  switch (p.bn) {
+    case 256: return launch_tc<256, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
+    case 128: return launch_tc<128, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
+    default: return launch_tc<64, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
+  }
 }
 
 // D[M x N] = A[az] . B[bz]^T, fused epilogue.  `splits` > 1 only with a partial epilogue.
@@ -485,7 +507,7 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
       return MLSTM_ECUDA;
     }
     cudaError_t e;
-    const int gflags = B.weight ? kGemmStaticB : 0;
+    const int gflags = B.weight ? (kGemmStaticB | kGemmRasterM) : 0;
     const PrefetchJob pj = pf.job;
     const CUtensorMap* ma2 = seg.A2 ? get_map(c, *seg.A2, 128) : ma;
     const CUtensorMap* mb2 = seg.B2 ? get_map(c, *seg.B2, p.pair ? p.bn / 2 : p.bn) : mb;
@@ -495,21 +517,17 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
     }
     const Seg2 sg{seg.A2 ? (K + 63) / 64 : (1 << 30), seg.az2, 0};
     const int Kt = seg.A2 ? ((K + 63) / 64) * 64 + seg.K2 : K;  // the kernels' K runs over both segments
-    if (p.cluster) {
-      e = p.splits == 2 ? launch_tc1s<2>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi)
-                        : launch_tc1s<4>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi);
-    } else if (p.pair) {
-      switch (p.bn) {
-        case 256: e = launch_tc2<256>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
-        case 128: e = launch_tc2<128>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
-        default: e = launch_tc2<64>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
+    if (A.mn != B.mn || (A.mn && seg.A2)) return fail(MLSTM_EINVAL, "gemm: mixed operand majors / MN segment");
+    if constexpr (kMNEpi<Epi>) {
+      if (A.mn) {
+        if (p.pair && p.bn < 128) return fail(MLSTM_EINVAL, "gemm: MN-major pair tiles need BN >= 128");
+        e = dispatch_tc<true>(c, p, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi);
+      } else {
+        e = dispatch_tc<false>(c, p, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi);
       }
     } else {
-      switch (p.bn) {
-        case 256: e = launch_tc<256>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
-        case 128: e = launch_tc<128>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
-        default: e = launch_tc<64>(c, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, p.splits, pj, epi); break;
-      }
+      if (A.mn) return fail(MLSTM_EINVAL, "gemm: MN-major operands only for weight-gradient epilogues");
+      e = dispatch_tc<false>(c, p, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi);
     }
     CUDA_OR_FAIL(c, e);
     return MLSTM_OK;
@@ -519,7 +537,7 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
   const S* b = static_cast<const S*>(B.ptr) + (long)bz * B.zstride;
   const int kps = (int)rup((K + p.splits - 1) / p.splits, 32);
   dim3 grid((N + 63) / 64, (M + 127) / 128, p.splits);
-  gemm_simt_kernel<S, Epi><<<grid, 128, 0, c->stream>>>(a, A.ld, b, B.ld, M, N, K, kps, epi);
+  gemm_simt_kernel<S, Epi><<<grid, 128, 0, c->stream>>>(a, A.ld, b, B.ld, M, N, K, kps, A.mn ? 1 : 0, epi);
   count_launch(c);
   CUDA_OR_FAIL(c, cudaGetLastError());
   return MLSTM_OK;
@@ -582,7 +600,8 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   const int h = c->h, e = c->e, B = c->B, T = c->T;
   phase(c, PH_PREP);
   LAUNCH(c, (state_in_kernel<S><<<grid_for((long)B * h), 256, 0, c->stream>>>(n, slot)));
-  if (n.OHR) LAUNCH(c, (onehot_kernel<S><<<grid_for((long)T * B), 256, 0, c->stream>>>(n)));
+  const bool fold = n.XZT != nullptr;  // tcgen05 path: W_x x + b enters F2 as a second K segment
+  if (fold) LAUNCH(c, (onehot_kernel<S><<<grid_for((long)T * B), 256, 0, c->stream>>>(n)));
   phase(c, PH_TAB);
   {
     Opd A{n.E_w, 256, e, e, 1, 256L * e};
@@ -594,7 +613,7 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   // W_h resident (evict_last); the activations are read once (evict_first).
   const Opd Hprev{n.Hrm, B, h, h, T + 1, (long)B * h, kPolFirst};
   const Opd Wmh{n.Wmh_w, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh), true};
-  const Opd Msc{n.Mscr, B, h, h, 1, (long)B * h, kPolFirst};
+  const Opd Mt{n.Mrm, B, h, h, T, (long)B * h, kPolFirst};  // m_t = slot t
   const Opd Wh{n.Wh_w, 4L * h, h, h, 1, 4L * h * h, pol_last(c->l2_wh), true};
   const Plan p1 = plan_gemm(c->tc, B, h, h, false), p2 = plan_gemm(c->tc, B, 4 * h, h + 256, false);
   // tcgen05 path: W_x x_t + b enters F2's accumulator as a second K segment, one-hot(bytes_t) x
@@ -602,7 +621,7 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   const Opd OH{n.OHR, B, 256, 256, T, (long)B * 256, kPolFirst};
   const Opd XZ{n.XZT, 4L * h, 256, 256, 1, 4L * h * 256, 0, true};
   Segment seg2;
-  if (n.OHR) {
+  if (fold) {
     seg2.A2 = &OH;
     seg2.B2 = &XZ;
     seg2.K2 = 256;
@@ -613,10 +632,10 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   for (int t = 0; t < T; ++t) {
     RET_IF(gemm<S>(c, Hprev, t, Wmh, 0, B, h, h, p1, EpiF1<S>{n, t}, pf1));
     seg2.az2 = t;
-    if (n.OHR && c->async_epi)  // tcgen05 path (W_x x + b folded): async row I/O epilogue
-      RET_IF(gemm<S>(c, Msc, 0, Wh, 0, B, 4 * h, h, p2, EpiF2IO<S>{{n, t, 1}, c->async_epi}, Prefetch{}, seg2));
+    if (fold && c->async_epi)  // tcgen05 path (W_x x + b folded): async row I/O epilogue
+      RET_IF(gemm<S>(c, Mt, t, Wh, 0, B, 4 * h, h, p2, EpiF2IO<S>{{n, t, 1}, c->async_epi}, Prefetch{}, seg2));
     else
-      RET_IF(gemm<S>(c, Msc, 0, Wh, 0, B, 4 * h, h, p2, EpiF2<S>{n, t, n.OHR != nullptr}, Prefetch{}, seg2));
+      RET_IF(gemm<S>(c, Mt, t, Wh, 0, B, 4 * h, h, p2, EpiF2<S>{n, t, fold ? 1 : 0}, Prefetch{}, seg2));
   }
   phase(c, PH_DEC);
   {
@@ -635,7 +654,7 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
   RET_IF(enqueue_forward<S>(c, MLSTM_SLOT_TRAIN));
   // the one-hot and the dC reset belong to the prep phase logically; they run here, off the
   // forward's critical path
-  if (!n.OHR) LAUNCH(c, (onehot_kernel<S><<<grid_for((long)T * B), 256, 0, c->stream>>>(n)));
+  if (!n.XZT) LAUNCH(c, (onehot_kernel<S><<<grid_for((long)T * B), 256, 0, c->stream>>>(n)));
   CUDA_OR_FAIL(c, cudaMemsetAsync(n.dC, 0, sizeof(float) * (size_t)B * h, c->stream));
   phase(c, PH_CE);
   const double denom = (double)c->Bfull * c->world * T;  // B_g * T (Q7): all rows of all ranks
@@ -661,9 +680,9 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
     segd.K2 = 256;
   }
   {
-    const Opd dZ{n.dZscr, B, 4L * h, 4L * h, 1, 4L * B * h, kPolFirst};
+    const Opd dZ{n.G5 + h, B, 4L * h, 5L * h, T, 5L * B * h, kPolFirst};  // dZ_t = slot t, cols [h, 5h)
     const Opd WhT{n.WhT, h, 4L * h, 4L * h, 1, 4L * h * h, pol_last(c->l2_wh), true};
-    const Opd dA{n.dAscr, B, h, h, 1, (long)B * h, kPolFirst};
+    const Opd dA{n.dA, B, h, h, T, (long)B * h, kPolFirst};
     const Opd WmhT{n.WmhT, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh), true};
     const Plan p1 = plan_gemm(c->tc, B, h, 4 * h, false), p2 = plan_gemm(c->tc, B, h, h, false);
     // B2 prefetches into L2 the first k-blocks (of each K split) of the W_h^T tiles B1 streams next
@@ -681,9 +700,9 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
         pb2.add(n.Astash + (long)(t - 1) * BH, BH * (long)es);
       }
       if (c->pf_bwd > 0 && c->tc) pb2.add(n.WhT, (long)(c->pf_bwd * 8.0 * h * h));
-      RET_IF(gemm<S>(c, dZ, 0, WhT, 0, B, h, 4 * h, p1, EpiB1<S>{n, t}, pb1));
+      RET_IF(gemm<S>(c, dZ, t, WhT, 0, B, h, 4 * h, p1, EpiB1<S>{n, t}, pb1));
       segd.az2 = t - 1;
-      if (t > 0) RET_IF(gemm<S>(c, dA, 0, WmhT, 0, B, h, h, p2, EpiB2<S>{n, t - 1}, pb2, segd));
+      if (t > 0) RET_IF(gemm<S>(c, dA, t, WmhT, 0, B, h, h, p2, EpiB2<S>{n, t - 1}, pb2, segd));
     }
   }
   phase(c, PH_WGRAD);
@@ -693,15 +712,13 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
       long M, N, off;
       int mode;
     };
+    // every operand MN-major: the row-major [T*B][cols] stashes the recurrence wrote, K = (t, b)
+    auto mn = [&](const void* p, long cols, long ld) { return Opd{p, cols, Kt, ld, 1, 0, 0, false, true}; };
     const W ws[4] = {
-        {{n.dGT + (long)h * c->ldK, 4L * h, Kt, c->ldK, 1, 4L * h * c->ldK}, {n.MT, h, Kt, c->ldK, 1, h * c->ldK},
-         4L * h, h, c->po.Wh, 1},                                                     // dW_h = dZ^T M
-        {{n.dAT, h, Kt, c->ldK, 1, h * c->ldK}, {n.HT, h, Kt, c->ldH, 1, h * c->ldH}, h, h, c->po.Wmh, 0},
-        // dW_mh = dA^T H_{t-1}
-        {{n.dYT, 256, Kt, c->ldK, 1, 256 * c->ldK}, {n.HT + c->Bp, h, Kt, c->ldH, 1, h * c->ldH}, 256, h,
-         c->po.Wdec, 0},                                                               // dW_dec = dY^T H
-        {{n.OHT, 256, Kt, c->ldK, 1, 256 * c->ldK}, {n.dGT, 5L * h, Kt, c->ldK, 1, 5L * h * c->ldK}, 256, 5L * h,
-         0, 2},                                                                        // S = onehot^T [dMX|dZ]
+        {mn(n.G5 + h, 4L * h, 5L * h), mn(n.Mrm, h, h), 4L * h, h, c->po.Wh, 1},      // dW_h = dZ^T M
+        {mn(n.dA, h, h), mn(n.Hrm, h, h), h, h, c->po.Wmh, 0},                         // dW_mh = dA^T H_{t-1}
+        {mn(n.dY, 256, 256), mn(n.Hrm + (long)B * h, h, h), 256, h, c->po.Wdec, 0},    // dW_dec = dY^T H
+        {mn(n.OHR, 256, 256), mn(n.G5, 5L * h, 5L * h), 256, 5L * h, 0, 2},          // S = onehot^T [dMX|dZ]
     };
     for (int wi = 0; wi < 4; ++wi) {
       const W& w = ws[wi];
@@ -1256,14 +1273,12 @@ mlstm_status mlstm_debug_dump(mlstm_ctx* c, const char* name, float* host_out, s
   if (nm == "onehot") {  // [256][T][B]
     const long cnt = 256 * T * B;
     if (!need(cnt)) return fail(MLSTM_EINVAL, "buffer too small");
-    std::vector<float> row(c->ldK);
-    const size_t es = c->mixed ? 2 : 4;
-    const uint8_t* base = c->mixed ? (const uint8_t*)c->nh.OHT : (const uint8_t*)c->nf.OHT;
-    for (int v = 0; v < 256; ++v) {
-      RET_IF(read_floats(c, base + es * v * c->ldK, c->ldK, row.data()));
+    std::vector<float> all(cnt);  // OHR is [T][B][256]
+    const uint8_t* base = c->mixed ? (const uint8_t*)c->nh.OHR : (const uint8_t*)c->nf.OHR;
+    RET_IF(read_floats(c, base, cnt, all.data()));
+    for (int v = 0; v < 256; ++v)
       for (long t = 0; t < T; ++t)
-        for (long b = 0; b < B; ++b) host_out[(v * T + t) * B + b] = row[t * c->Bp + b];
-    }
+        for (long b = 0; b < B; ++b) host_out[(v * T + t) * B + b] = all[(t * B + b) * 256 + v];
     return MLSTM_OK;
   }
   return fail(MLSTM_EINVAL, "unknown dump name");

@@ -69,8 +69,6 @@ template <typename S>
 struct Net {
   int h, e, B, T, Bp;
   int Bfull, nmb;  // rows per rank and micro-batches per step (B = Bfull / nmb rows per micro-batch)
-  long ldK;  // leading dim of the transposed stashes over K = T*Bp (padded to 64)
-  long ldH;  // leading dim of HT over (T+1)*Bp
   ParamOffsets po;
   const uint8_t* bytes;  // [B][T+1]
   const uint8_t* reset;  // [B] or null
@@ -81,25 +79,21 @@ struct Net {
   // activations / stash
   float* tab;     // [256][5h]: cols [0,h) = W_mx E^T (mx table), [h,5h) = W_x E^T in internal order
   S* XZT;         // [4h][256] (W_x E^T + b)^T in internal row order: F2's second K segment (mixed mode)
-  S* OHR;         // [T][B][256] one-hot of the input bytes, row-major: F2's second A segment
+  S* OHR;         // [T][B][256] one-hot of the input bytes: F2's second A segment (tcgen05 path) and the
+                  // MN-major A operand of the per-byte sums S = onehot^T [dMX | dZ]
   S* Hrm;         // [(T+1)][B][h]; block 0 = h0, block t+1 = H_t
-  S* HT;          // [h][ldH]; column t*Bp+b = Hrm[t][b]
   float* Crm;     // [(T+1)][B][h]
-  S* Mscr;        // [B][h]   m_t of the current step (A operand of the W_h GEMM)
-  S* MT;          // [h][ldK] m_t^T stash (B operand of dW_h)
+  S* Mrm;         // [T][B][h] m_t: A operand of F2 at t; MN-major B operand of dW_h = dZ^T M
   S* Astash;      // [T][B][h] a_t = W_mh h_{t-1}
   S* Gates;       // [T][B][4h] i,f,o,u activations, internal order
   float* Y;       // [T*B][256] logits (fp32)
   float* lossrow; // [T*B]
   S* dY;          // [T*B][256]
-  S* dYT;         // [256][ldK]
-  S* OHT;         // [256][ldK] one-hot of the input bytes, transposed
   float* dHdec;   // [T*B][h] (SIMT path only; null when B2 folds dY W_dec into its K loop)
-  S* dZscr;       // [B][4h] internal order
-  S* dAscr;       // [B][h]
+  S* G5;          // [T][B][5h]: cols [0,h) dMX, [h,5h) dZ (internal order); dZ_t is B1's A operand,
+                  // the whole stash the MN-major operand of dW_h (dZ) and of the per-byte sums
+  S* dA;          // [T][B][h] dA_t: B2's A operand at t; MN-major A operand of dW_mh
   float* dC;      // [B][h] dc carry
-  S* dGT;         // [5h][ldK]: rows [0,h) dMX^T, rows [h,5h) dZ^T (internal)
-  S* dAT;         // [h][ldK]
   float* part;    // split-K partials
   float* Scan;    // [256][5h] per-byte segmented sums, canonical columns
   S* hstate;      // [2][Bfull][h]  persisted h per slot
@@ -109,7 +103,6 @@ struct Net {
   float* colsum_part;
   DevState* st;
   __device__ __forceinline__ int byte_at(int b, int t) const { return bytes[(long)b * (T + 1) + t]; }
-  __device__ __forceinline__ long kcol(int t, int b) const { return (long)t * Bp + b; }
 };
 
 template <typename S>

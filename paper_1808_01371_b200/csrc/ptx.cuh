@@ -156,11 +156,25 @@ __device__ __forceinline__ uint64_t sdesc_kmajor_sw128(uint32_t smem_addr) {
   d |= static_cast<uint64_t>(2) << 61;                     // SWIZZLE_128B
   return d;
 }
-// Instruction descriptor: kind::f16, A = B = fp16, D = fp32, both K-major, shape M x N.
-__host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N) {
+// UMMA shared-memory descriptor for an MN-major operand tile stored with the 128-byte swizzle: TMA
+// boxes of 64 MN-contiguous fp16 (128 B) x 64 K rows (8 KB each, 1024-byte aligned), one box per 64
+// MN elements.  Canonical layout ((8,8,m),(8,k)) : ((1,8,LBO),(64,SBO)) elements: LBO = 8192 B
+// between 64-wide MN blocks, SBO = 1024 B between 8-row K groups; advancing K by 16 adds 2048 B.
+__device__ __forceinline__ uint64_t sdesc_mnmajor_sw128(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr & 0x3FFFF) >> 4);  // start address   [0,14)
+  d |= static_cast<uint64_t>(8192 >> 4) << 16;             // LBO             [16,30)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;             // SBO             [32,46)
+  d |= static_cast<uint64_t>(1) << 46;                     // descriptor version = 1
+  d |= static_cast<uint64_t>(2) << 61;                     // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor: kind::f16, A = B = fp16, D = fp32, shape M x N; both operands K-major,
+// or both MN-major (transpose bits 15/16).
+__host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N, bool mn = false) {
   return (1u << 4)                                  // D format: F32
          | (0u << 7) | (0u << 10)                   // A, B format: F16
-         | (0u << 15) | (0u << 16)                  // A, B K-major
+         | ((mn ? 1u : 0u) << 15) | ((mn ? 1u : 0u) << 16)  // A, B major-ness
          | (static_cast<uint32_t>(N >> 3) << 17)    // N / 8
          | (static_cast<uint32_t>(M >> 4) << 24);   // M / 16
 }
