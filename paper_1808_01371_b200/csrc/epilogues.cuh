@@ -124,6 +124,45 @@ __device__ __forceinline__ void warp_rows_out(uint8_t* dst, long dpitch, const u
   }
 }
 
+// Stage this lane's 16*NG-value row piece (converted to S) in the warp window and store the warp's
+// rows coalesced: dst0 = the row of lane 0, consecutive rows `pitch` elements apart.
+template <int NG, typename S>
+__device__ __forceinline__ void stage_rows_out(const EpiIO& io, S* dst0, long pitch, const float* vals) {
+  constexpr int BYTES = 16 * NG * (int)sizeof(S);
+  S* w = reinterpret_cast<S*>(io.buf + io.lane * (BYTES + 16));
+#pragma unroll
+  for (int q = 0; q < NG; ++q) st16(w + 16 * q, vals + 16 * q);
+  warp_rows_out(reinterpret_cast<uint8_t*>(dst0), pitch * (long)sizeof(S), io.buf, BYTES + 16, BYTES, io.nvalid,
+                io.lane);
+  __syncwarp();
+}
+
+// Row-I/O forms of EpiF1 / EpiB1: same loads, outputs staged and stored coalesced.
+template <typename S>
+struct EpiF1IO : EpiF1<S> {
+  static constexpr bool kAsyncIO = true;
+  __device__ __forceinline__ void io_issue(const EpiIO&, int, int) const {}
+  template <int NG>
+  __device__ __forceinline__ void run_io(const EpiIO& io, int, int col0, const float* v) const {
+    const Net<S>& n = this->n;
+    const int t = this->t, b = io.row0 + io.lane;
+    float m[16 * NG];
+    if (io.valid()) {
+      const float* mx = n.tab + (long)n.byte_at(b, t) * 5 * n.h + col0;
+#pragma unroll
+      for (int q = 0; q < NG; ++q) {
+        float x[16];
+        ld16(mx + 16 * q, x);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) m[16 * q + i] = x[i] * v[16 * q + i];
+      }
+    }
+    const long r0 = (long)t * n.B + io.row0;
+    stage_rows_out<NG>(io, n.Mrm + r0 * n.h + col0, n.h, m);
+    stage_rows_out<NG>(io, n.Astash + r0 * n.h + col0, n.h, v);
+  }
+};
+
 template <typename S>
 struct EpiF2IO : EpiF2<S> {
   static constexpr bool kAsyncIO = true;
@@ -293,6 +332,36 @@ struct EpiB1 {
   }
 };
 
+
+template <typename S>
+struct EpiB1IO : EpiB1<S> {
+  static constexpr bool kAsyncIO = true;
+  __device__ __forceinline__ void io_issue(const EpiIO&, int, int) const {}
+  template <int NG>
+  __device__ __forceinline__ void run_io(const EpiIO& io, int, int col0, const float* v) const {
+    const Net<S>& n = this->n;
+    const int t = this->t, b = io.row0 + io.lane;
+    float da[16 * NG], dmx[16 * NG];
+    if (io.valid()) {
+      const float* mx = n.tab + (long)n.byte_at(b, t) * 5 * n.h + col0;
+      const S* arow = n.Astash + ((long)t * n.B + b) * n.h + col0;
+#pragma unroll
+      for (int q = 0; q < NG; ++q) {
+        float x[16], a[16];
+        ld16(mx + 16 * q, x);
+        ld16(arow + 16 * q, a);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          da[16 * q + i] = v[16 * q + i] * x[i];
+          dmx[16 * q + i] = v[16 * q + i] * a[i];
+        }
+      }
+    }
+    const long r0 = (long)t * n.B + io.row0;
+    stage_rows_out<NG>(io, n.dA + r0 * n.h + col0, n.h, da);
+    stage_rows_out<NG>(io, n.G5 + r0 * 5 * n.h + col0, 5L * n.h, dmx);
+  }
+};
 
 // Cooperative tile form of the gate backward (used by the split-K engine, whose reduced fp32 tile
 // T[rows][U] (row stride ldt, columns = hidden units n0..n0+U) sits in shared memory).  The row-

@@ -183,8 +183,8 @@ __device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUten
   };
   auto loadB = [&](int s, int kb) {
     if constexpr (MN) {
-#pragma unroll
       static_assert(!MN || C::B_BYTES % 8192 == 0, "MN-major B needs 64-wide boxes per CTA");
+#pragma unroll
       for (int i = 0; i < C::B_BYTES / 8192; ++i) {
         uint8_t* dst = L.sB + s * C::B_BYTES + i * 8192;
         if (PAIR) ptx::tma_load_3d_2sm(dst, tmB, bar_leader0 + s * 8, nb0 + 64 * i, kb * C::BK, bz, pb);

@@ -26,6 +26,8 @@ namespace mlstm {  // trace tags of the fused epilogues (mlstm_trace_read)
 template <typename S> struct EpiTag<EpiF1<S>> { static constexpr int value = 1; };
 template <typename S> struct EpiTag<EpiF2<S>> { static constexpr int value = 2; };
 template <typename S> struct EpiTag<EpiF2IO<S>> { static constexpr int value = 2; };
+template <typename S> struct EpiTag<EpiF1IO<S>> { static constexpr int value = 1; };
+template <typename S> struct EpiTag<EpiB1IO<S>> { static constexpr int value = 3; };
 template <typename S> struct EpiTag<EpiB1<S>> { static constexpr int value = 3; };
 template <typename S> struct EpiTag<EpiB2<S>> { static constexpr int value = 4; };
 template <typename S> struct EpiTag<EpiY<S>> { static constexpr int value = 5; };
@@ -630,7 +632,10 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   Prefetch pf1;
   if (c->pf_fwd > 0 && c->tc) pf1.add(n.Wh_w, (long)(c->pf_fwd * 8.0 * h * h));
   for (int t = 0; t < T; ++t) {
-    RET_IF(gemm<S>(c, Hprev, t, Wmh, 0, B, h, h, p1, EpiF1<S>{n, t}, pf1));
+    if (fold && c->async_epi)
+      RET_IF(gemm<S>(c, Hprev, t, Wmh, 0, B, h, h, p1, EpiF1IO<S>{{n, t}}, pf1));
+    else
+      RET_IF(gemm<S>(c, Hprev, t, Wmh, 0, B, h, h, p1, EpiF1<S>{n, t}, pf1));
     seg2.az2 = t;
     if (fold && c->async_epi)  // tcgen05 path (W_x x + b folded): async row I/O epilogue
       RET_IF(gemm<S>(c, Mt, t, Wh, 0, B, 4 * h, h, p2, EpiF2IO<S>{{n, t, 1}, c->async_epi}, Prefetch{}, seg2));
@@ -700,7 +705,10 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
         pb2.add(n.Astash + (long)(t - 1) * BH, BH * (long)es);
       }
       if (c->pf_bwd > 0 && c->tc) pb2.add(n.WhT, (long)(c->pf_bwd * 8.0 * h * h));
-      RET_IF(gemm<S>(c, dZ, t, WhT, 0, B, h, 4 * h, p1, EpiB1<S>{n, t}, pb1));
+      if (c->tc && c->async_epi)
+        RET_IF(gemm<S>(c, dZ, t, WhT, 0, B, h, 4 * h, p1, EpiB1IO<S>{{n, t}}, pb1));
+      else
+        RET_IF(gemm<S>(c, dZ, t, WhT, 0, B, h, 4 * h, p1, EpiB1<S>{n, t}, pb1));
       segd.az2 = t - 1;
       if (t > 0) RET_IF(gemm<S>(c, dA, t, WmhT, 0, B, h, h, p2, EpiB2<S>{n, t - 1}, pb2, segd));
     }
