@@ -94,7 +94,7 @@ struct mlstm_ctx {
   int seg_splits = 1;
   float l2_wmh = 0.f, l2_wh = 0.f;  // evict_last fractions of the recurrent weights
   float* split_scratch = nullptr;
-  bool pdl = false;                   // programmatic dependent launch of the GEMMs (MLSTM_PDL=1; neutral)
+  bool pdl = true;                    // programmatic dependent launch of the GEMMs (MLSTM_PDL=0 disables)
   float pf_fwd = 0.f, pf_bwd = 0.f;   // L2 prefetch of the next W_h / W_h^T (MLSTM_PF_FWD/BWD; neutral,
                                       // profiles/r01_l2_prefetch.log)
   bool pf_stash = true;               // backward: prefetch the next epilogue's stash blocks (MLSTM_PF_STASH)
