@@ -494,6 +494,163 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 }
 
 // ---------------------------------------------------------------------------------------------
+// Persistent CTA-pair engine for GEMMs with more 256 x BN tiles than pairs fit on the GPU: the grid
+// holds min(tiles, max_pairs) pairs and pair p walks tiles p, p + npairs, ...  The TMEM accumulator
+// is double-buffered (2 x BN columns), so the epilogue of tile i overlaps the main loop of tile
+// i+1; the stage ring and its phases run on across tiles.  Barriers (leader CTA unless noted):
+// acc_full[b] (MMA commit, multicast to both CTAs) and acc_empty[b] (one arrive per epilogue warp
+// of both CTAs, the peer's remotely).  Epilogues run in their row form (run<NG>).
+template <int BN, class Epi, bool MN = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    gemm_tc2p_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, Seg2 sg,
+                     int M, int N, int K, int az, int bz, int unused, uint32_t polA, uint32_t polB, int flags,
+                     PrefetchJob pj, Epi epi) {
+  using C = Tc2Cfg<BN>;
+  static_assert(2 * BN <= 512, "two accumulators must fit in TMEM");
+  extern __shared__ uint8_t smem_raw[];
+  const SmemLayout<C> L(smem_raw);
+  uint64_t* acc_full = L.epibar;       // [2]
+  uint64_t* acc_empty = L.epibar + 2;  // [2]
+  MLSTM_TRACE_BEGIN();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int mt = (M + 255) / 256, nt = (N + BN - 1) / BN, ntiles = mt * nt;
+  const int pid = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const bool rm = flags & kGemmRasterM;
+  const int total_kb = (K + C::BK - 1) / C::BK;
+  auto tile_m = [&](int tile) { return (rm ? tile % mt : tile / nt) * 256 + (int)rank * 128; };
+  auto tile_n = [&](int tile) { return (rm ? tile / mt : tile % nt) * BN; };
+  if (threadIdx.x == 0) {
+#pragma unroll 1
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(&L.full[s], 1);
+      ptx::mbar_init(&L.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&acc_full[b], 1);
+      ptx::mbar_init(&acc_empty[b], 2 * kEpiWarps);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) {
+    ptx::tmem_alloc2(L.tmem_slot, 2 * BN);
+    ptx::tmem_relinquish2();
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *L.tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pa = ptx::make_policy(polA), pb = ptx::make_policy(polB);
+      const uint32_t tx = 2 * C::STAGE_BYTES;
+      const uint32_t bar0 = ptx::mapa_shared(ptx::smem_u32(&L.full[0]), 0);
+      ptx::pdl_wait();
+      if (tracing) tr_ts[1] = ptx::globaltimer();
+      int it = 0;
+#pragma unroll 1
+      for (int tile = pid; tile < ntiles; tile += npairs) {
+        const int m0 = tile_m(tile), nb0 = tile_n(tile) + (int)rank * (BN / 2);
+#pragma unroll 1
+        for (int kb = 0; kb < total_kb; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          if (it >= C::STAGES) ptx::mbar_wait(&L.empty[s], ((it / C::STAGES) & 1) ^ 1);
+          if (leader) ptx::mbar_arrive_expect_tx(&L.full[s], tx);
+          uint8_t* da = L.sA + s * C::A_BYTES;
+          uint8_t* db = L.sB + s * C::B_BYTES;
+          if constexpr (MN) {
+#pragma unroll
+            for (int i = 0; i < C::BM / 64; ++i)
+              ptx::tma_load_3d_2sm(da + i * 8192, &tmA, bar0 + s * 8, m0 + 64 * i, kb * C::BK, az, pa);
+            static_assert(!MN || C::B_BYTES % 8192 == 0, "MN-major B needs 64-wide boxes per CTA");
+#pragma unroll
+            for (int i = 0; i < C::B_BYTES / 8192; ++i)
+              ptx::tma_load_3d_2sm(db + i * 8192, &tmB, bar0 + s * 8, nb0 + 64 * i, kb * C::BK, bz, pb);
+          } else {
+            const bool s2 = kb >= sg.kb_seg0;
+            const int k = (s2 ? kb - sg.kb_seg0 : kb) * C::BK;
+            ptx::tma_load_3d_2sm(da, s2 ? &tmA2 : &tmA, bar0 + s * 8, k, m0, s2 ? sg.az2 : az, pa);
+            ptx::tma_load_3d_2sm(db, s2 ? &tmB2 : &tmB, bar0 + s * 8, k, nb0, s2 ? sg.bz2 : bz, pb);
+          }
+        }
+      }
+      l2_prefetch(pj);
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_f16_f32(256, BN, MN);
+      constexpr int kstep = MN ? 2048 >> 4 : 32 >> 4;
+      int it = 0, lt = 0;
+#pragma unroll 1
+      for (int tile = pid; tile < ntiles; tile += npairs, ++lt) {
+        const int b = lt & 1, use = lt >> 1;
+        if (use > 0) ptx::mbar_wait(&acc_empty[b], (use - 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t td = tmem + b * BN;
+#pragma unroll 1
+        for (int kb = 0; kb < total_kb; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          ptx::mbar_wait(&L.full[s], (it / C::STAGES) & 1);
+          ptx::tc_fence_after();
+          if (tracing && it == 0) tr_ts[2] = ptx::globaltimer();
+          const uint32_t sa = ptx::smem_u32(L.sA + s * C::A_BYTES), sb = ptx::smem_u32(L.sB + s * C::B_BYTES);
+          const uint64_t ad = MN ? ptx::sdesc_mnmajor_sw128(sa) : ptx::sdesc_kmajor_sw128(sa);
+          const uint64_t bd = MN ? ptx::sdesc_mnmajor_sw128(sb) : ptx::sdesc_kmajor_sw128(sb);
+#pragma unroll
+          for (int k = 0; k < C::BK / 16; ++k)
+            ptx::mma_f16_2sm(td, ad + kstep * k, bd + kstep * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          ptx::mma_commit_2sm_mc(&L.empty[s], 0x3);
+        }
+        ptx::mma_commit_2sm_mc(&acc_full[b], 0x3);
+      }
+    }
+  } else {
+    const int q = warp & 3, grp = (warp - 2) >> 2;
+    const uint32_t empty_addr0 = ptx::mapa_shared(ptx::smem_u32(&acc_empty[0]), 0);
+    int lt = 0;
+#pragma unroll 1
+    for (int tile = pid; tile < ntiles; tile += npairs, ++lt) {
+      const int b = lt & 1, use = lt >> 1;
+      ptx::mbar_wait(&acc_full[b], use & 1);
+      ptx::tc_fence_after();
+      if (lt == 0) {
+        if (tracing && threadIdx.x == 64) tr_ts[3] = ptx::globaltimer();
+        ptx::pdl_wait();
+      }
+      if (tile + npairs >= ntiles && threadIdx.x == 64) ptx::pdl_trigger();  // last tile of this pair
+      const int m0 = tile_m(tile), n0 = tile_n(tile);
+      const int row = m0 + q * 32 + lane;
+#pragma unroll 1
+      for (int c = grp; c < BN / 64; c += 2) {
+        float v[64];
+        tmem_chunk(tmem + b * BN, q, c, true, v);
+        const int col0 = n0 + c * 64;
+        if (row < M && col0 < N) epi.template run<4>(row, col0, v);
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) ptx::mbar_arrive(&acc_empty[b]);
+        else ptx::mbar_arrive_remote(empty_addr0 + b * 8);
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  MLSTM_TRACE_END();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc2(tmem, 2 * BN);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Split-K over a cluster of S CTAs (rank z = K split).  Each CTA writes its fp32 partial to an
 // L2-resident scratch laid out [z][float4 column group (64)][row (128)] (lanes = rows: coalesced);
 // after the cluster barrier (release/acquire at cluster scope orders those writes) CTA z sums

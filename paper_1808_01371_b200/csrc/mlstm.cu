@@ -63,6 +63,7 @@ struct Plan {
   int bn, splits;
   bool pair;     // CTA-pair (cta_group::2) 256-row tiles
   bool cluster;  // K split over the CTAs of a cluster, reduced in-kernel (1-CTA 128 x 256 tiles)
+  bool persist = false;  // pair tiles walked by a persistent grid (more tiles than pairs fit)
 };
 constexpr long kSplitScratchFloats = 160L * 128 * 256;  // >= tiles * S partials of any cluster-split plan
 
@@ -180,18 +181,21 @@ int grid_for(long n, int threads = 256, int cap = 148 * 16) {
 // Test instrument (MLSTM_FORCE_PLAN=pair|split|single): take one tile plan wherever it is legal, so
 // small parity tests cover the plans that only full-size shapes select on their own.
 int g_force_plan = 0;
+int g_max_pairs = 74;  // CTA pairs resident at once (148 SMs); MLSTM_PERSIST_PAIRS overrides (tests)
 
 Plan plan_gemm(bool tc, long M, long N, long K, bool allow_split) {
   Plan p{64, 1, false, false};
   const long kb = (K + 63) / 64;
-  if (tc && g_force_plan == 1 && M > 128) return Plan{256, 1, true, false};
+  const long pairs = ((M + 255) / 256) * ((N + 255) / 256);
+  if (tc && g_force_plan == 1 && M > 128) return Plan{256, 1, true, false, pairs > g_max_pairs};
+  if (tc && g_force_plan == 4 && M > 128) return Plan{256, 1, true, false, true};
   if (tc && g_force_plan == 2 && kb >= 8) {
     const int sp = kb >= 16 ? 4 : 2;
     if (((M + 127) / 128) * ((N + 255) / 256) * sp <= 160) return Plan{256, sp, false, true};
   }
   if (tc && g_force_plan == 3) allow_split = false;
   if (tc && g_force_plan != 0) goto single;
-  if (tc && M > 128 && ((M + 255) / 256) * ((N + 255) / 256) >= 60) return Plan{256, 1, true, false};
+  if (tc && M > 128 && pairs >= 60) return Plan{256, 1, true, false, pairs > g_max_pairs};
   if (tc) {
     const long mt = (M + 127) / 128;
     // 128 x 256 tiles with the K loop split over a cluster of S <= 4 CTAs when 256-wide tiles
@@ -326,7 +330,9 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   {
     const char* v = getenv("MLSTM_FORCE_PLAN");
     const std::string fp = v ? v : "";
-    c->force_plan = fp == "pair" ? 1 : fp == "split" ? 2 : fp == "single" ? 3 : 0;
+    c->force_plan = fp == "pair" ? 1 : fp == "split" ? 2 : fp == "single" ? 3 : fp == "persist" ? 4 : 0;
+    const char* pp = getenv("MLSTM_PERSIST_PAIRS");
+    g_max_pairs = pp ? std::max(1, atoi(pp)) : 74;
   }
   const char* dbg = getenv("MLSTM_DEBUG_SIMT_GEMM");  // test instrument: mixed mode on the SIMT engine
   c->tc = c->mixed && !(dbg && dbg[0] == '1');
@@ -451,6 +457,16 @@ cudaError_t launch_tc2(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* m
                      Tc2Cfg<BN>::SMEM, 2, *ma, *mb, *ma2, *mb2, sg, M, N, K, az, bz, kbps, pa, pb, flags, pj, epi);
 }
 
+template <int BN, class Epi, bool MN = false>
+cudaError_t launch_tc2p(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, const CUtensorMap* ma2,
+                        const CUtensorMap* mb2, Seg2 sg, int M, int N, int K, int az, int bz, uint32_t pa,
+                        uint32_t pb, int flags, PrefetchJob pj, const Epi& epi) {
+  const int tiles = ((M + 255) / 256) * ((N + BN - 1) / BN);
+  const int npairs = std::min(tiles, g_max_pairs);
+  return launch_gemm(c, gemm_tc2p_kernel<BN, Epi, MN>, dim3(2 * npairs, 1, 1), Tc2Cfg<BN>::SMEM, 2, *ma, *mb, *ma2,
+                     *mb2, sg, M, N, K, az, bz, 0, pa, pb, flags, pj, epi);
+}
+
 // Engine dispatch for one plan (MN: both operands MN-major).
 template <bool MN, class Epi>
 cudaError_t dispatch_tc(mlstm_ctx* c, const Plan& p, const CUtensorMap* ma, const CUtensorMap* mb,
@@ -459,6 +475,8 @@ cudaError_t dispatch_tc(mlstm_ctx* c, const Plan& p, const CUtensorMap* ma, cons
   if (p.cluster)
     return p.splits == 2 ? launch_tc1s<2, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, pj, epi)
                          : launch_tc1s<4, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, pj, epi);
+  if (p.pair && p.persist && p.splits == 1)
+    return launch_tc2p<256, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, pj, epi);
   if (p.pair) {
     if (MN || p.bn == 256)
       return launch_tc2<256, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);

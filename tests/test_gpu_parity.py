@@ -252,13 +252,15 @@ def test_micro_batches_equal_one_batch(precision):
     assert rel_l2(split.get_params().astype(np.float64), whole.get_params().astype(np.float64)) < 1e-4
 
 
-@pytest.mark.parametrize("plan", ["pair", "split", "single"])
+@pytest.mark.parametrize("plan", ["pair", "split", "single", "persist"])
 @pytest.mark.parametrize("h,B,T", [(512, 256, 4), (512, 200, 3), (1024, 256, 2)])
 def test_forced_tile_plans_match_oracle(plan, h, B, T, monkeypatch):
-    """Every tcgen05 tile plan (CTA pair, cluster split-K, single CTA) on every GEMM of the step,
+    """Every tcgen05 tile plan (CTA pair, cluster split-K, single CTA, persistent pairs) on every GEMM,
     forced at a size the oracle finishes quickly (full-size shapes select them on their own);
     B=200 leaves a ragged last M tile."""
     monkeypatch.setenv("MLSTM_FORCE_PLAN", plan)
+    if plan == "persist":  # two resident pairs: every pair walks several tiles (TMEM double buffer)
+        monkeypatch.setenv("MLSTM_PERSIST_PAIRS", "2")
     e = 64
     m = make_model(h, e, B, T, "mixed")
     theta0 = m.get_params().astype(np.float64)
