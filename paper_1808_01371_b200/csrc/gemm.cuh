@@ -162,7 +162,10 @@ __device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUten
                                              const CUtensorMap* tmA2, const CUtensorMap* tmB2, Seg2 sg, int nkb,
                                              int kb0, int m0, int nb0, int az, int bz, uint32_t polA,
                                              uint32_t polB, int flags, bool leader, uint32_t bar_leader0,
-                                             uint64_t* trace_slot) {
+                                             uint64_t* trace_slot, int part = 0) {
+  // part 0: everything; part 1: only the static-B stages (issued by the barrier-initialising thread
+  // before the CTA-wide setup barrier, so the weight stream starts while TMEM is being allocated);
+  // part 2: everything but those stages.
   const uint64_t pa = ptx::make_policy(polA), pb = ptx::make_policy(polB);
   const uint32_t tx = PAIR ? 2 * C::STAGE_BYTES : C::STAGE_BYTES;
   auto loadA = [&](int s, int kb) {
@@ -199,10 +202,12 @@ __device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUten
     else ptx::tma_load_3d(L.sB + s * C::B_BYTES, m, &L.full[s], k, nb0, z, pb);
   };
   const int pre = (flags & kGemmStaticB) ? min(C::STAGES, nkb) : 0;
-  for (int i = 0; i < pre; ++i) {
-    if (leader) ptx::mbar_arrive_expect_tx(&L.full[i], tx);
-    loadB(i, kb0 + i);
-  }
+  if (part != 2)
+    for (int i = 0; i < pre; ++i) {
+      if (leader) ptx::mbar_arrive_expect_tx(&L.full[i], tx);
+      loadB(i, kb0 + i);
+    }
+  if (part == 1) return;
   ptx::pdl_wait();
   if (trace_slot) *trace_slot = ptx::globaltimer();
   for (int i = 0; i < pre; ++i) loadA(i, kb0 + i);
@@ -365,6 +370,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int kb0 = blockIdx.z * kb_per_split;
   const int nkb = max(0, min(kb_per_split, total_kb - kb0));
   gemm_setup<C, false>(L, &tmA, &tmB, BN);
+  if (threadIdx.x == 0 && nkb > 0)  // the barrier-initialising thread starts the weight stream
+    gemm_produce<C, false, MN>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true, 0,
+                               nullptr, 1);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -373,7 +381,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       if (nkb > 0)
         gemm_produce<C, false, MN>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true,
-                                   0, MLSTM_TRACE_SLOT(1));
+                                   0, MLSTM_TRACE_SLOT(1), 2);
       l2_prefetch(pj);
     }
   } else if (warp == 1) {
@@ -440,6 +448,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int kb0 = blockIdx.z * kb_per_split;
   const int nkb = max(0, min(kb_per_split, total_kb - kb0));
   gemm_setup<C, true>(L, &tmA, &tmB, BN);
+  // the leader's own static-B stages can start before the cluster barrier (they complete on its own
+  // barriers); the peer's signal the leader's barriers, so they wait for it
+  if (leader && threadIdx.x == 0 && nkb > 0)
+    gemm_produce<C, true, MN>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true,
+                              ptx::mapa_shared(ptx::smem_u32(&L.full[0]), 0), nullptr, 1);
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
@@ -448,7 +461,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       if (nkb > 0)
         gemm_produce<C, true, MN>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0 + rank * (BN / 2), az, bz, polA, polB, flags,
-                              leader, ptx::mapa_shared(ptx::smem_u32(&L.full[0]), 0), MLSTM_TRACE_SLOT(1));
+                              leader, ptx::mapa_shared(ptx::smem_u32(&L.full[0]), 0), MLSTM_TRACE_SLOT(1),
+                              leader ? 2 : 0);
       l2_prefetch(pj);
     }
   } else if (warp == 1) {
@@ -688,6 +702,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   float* part = scratch + ((long)(blockIdx.y * (gridDim.x / S) + tile_n) * S) * (128L * BN);
   float* stageT = reinterpret_cast<float*>(L.sA);  // tile-epilogue staging: the stages are idle by then
   gemm_setup<C, false>(L, &tmA, &tmB, BN);
+  if (threadIdx.x == 0 && nkb > 0)  // the barrier-initialising thread starts the weight stream
+    gemm_produce<C, false, MN>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true, 0,
+                               nullptr, 1);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -696,7 +713,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       if (nkb > 0)
         gemm_produce<C, false, MN>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0, az, bz, polA, polB, flags, true,
-                                   0, MLSTM_TRACE_SLOT(1));
+                                   0, MLSTM_TRACE_SLOT(1), 2);
       l2_prefetch(pj);
     }
   } else if (warp == 1) {
