@@ -22,6 +22,8 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
   * overflow     -- IEEE binary16 thresholds (65504 finite, 65520 -> inf).
   * init         -- SplitMix64 published reference outputs.
   * speedup      -- Tab. gpu_scale (P:215-228) arithmetic.
+  * weight norm  -- S:129-130 worked examples, finite differences through (v, g), scale
+                    invariance in v, dv orthogonal to v, function-preserving init.
 No function is "parity unpinned".
 """
 from __future__ import annotations
@@ -348,25 +350,31 @@ class TrainState:
     it: int = 0                       # LR clock: advances every step incl. skipped (Q10)
     h_state: np.ndarray | None = None
     c_state: np.ndarray | None = None
+    weight_norm: bool = False         # theta in the wn layout (v, gains)
 
 
-def new_train_state(h: int, e: int, B: int, seed: int, scaler: ScalerState | None = None) -> TrainState:
-    theta = flatten(init_params(h, e, seed))
+def new_train_state(h: int, e: int, B: int, seed: int, scaler: ScalerState | None = None,
+                    weight_norm: bool = False) -> TrainState:
+    theta = wn_init(h, e, seed) if weight_norm else flatten(init_params(h, e, seed))
     return TrainState(h, e, theta, AdamState(np.zeros_like(theta), np.zeros_like(theta)),
-                      scaler or ScalerState(), 0, np.zeros((B, h)), np.zeros((B, h)))
+                      scaler or ScalerState(), 0, np.zeros((B, h)), np.zeros((B, h)), weight_norm)
 
 
 def train_step(st: TrainState, bytes_, lr0=3e-3, decay_iters=100_000, n_global_rows=None,
                reset=None, grads_hook=None, loss_hook=None, beta1=0.9, beta2=0.999, eps=1e-8):
     """Returns a dict {loss_nats, bpc, skipped, alpha, lr, grads (unscaled, flat)}; mutates st."""
-    P = unflatten(st.theta, st.h, st.e)
     bytes_ = np.asarray(bytes_)
     Bn, T1 = bytes_.shape
     Bg = Bn if n_global_rows is None else n_global_rows
     alpha = st.scaler.alpha
-    loss_sum, grads, (hT, cT), _ = loss_and_grads(P, bytes_, st.h_state, st.c_state, Bg, alpha,
-                                                 reset=reset)
-    gflat = flatten(grads)                      # alpha-scaled, mean over global positions
+    if st.weight_norm:
+        loss_sum, gflat, (hT, cT), _ = wn_loss_and_grads(st.theta, st.h, st.e, bytes_, st.h_state, st.c_state,
+                                                         Bg, alpha, reset=reset)
+    else:
+        P = unflatten(st.theta, st.h, st.e)
+        loss_sum, grads, (hT, cT), _ = loss_and_grads(P, bytes_, st.h_state, st.c_state, Bg, alpha,
+                                                     reset=reset)
+        gflat = flatten(grads)                  # alpha-scaled, mean over global positions
     if grads_hook is not None:
         gflat = grads_hook(gflat)               # e.g. SUM allreduce across ranks (Q7)
     if loss_hook is not None:
@@ -389,6 +397,87 @@ def evaluate(P: dict, bytes_, h0, c0, reset=None):
     loss_sum, cache, state = forward(P, bytes_, h0, c0, reset=reset)
     Bn, T1 = np.asarray(bytes_).shape
     return loss_sum, Bn * (T1 - 1), state
+
+
+# --------------------------------------------------------------------------------------
+# Weight normalisation (P:149-150 [§VI "Weight Normalization"]: applied "to the LSTM parameters
+# only ... the 4 hidden->hidden and input->hidden parameters", not to biases; Salimans & Kingma
+# 2016; S:124-131 weight_norm_build).  Row-wise over output units: w_i = g_i v_i / ||v_i||_2.
+# Parameters become v (in the W slots of the canonical layout) and one gain per row, appended
+# after b_dec in the order g_mx[h] | g_mh[h] | g_x[4h] | g_h[4h] (reading Q24).  Init: v as the
+# plain init, g_i = ||v_i|| (function-preserving; paper silent).
+# --------------------------------------------------------------------------------------
+
+WN_NAMES = ("W_mx", "W_mh", "W_x", "W_h")
+
+
+def wn_gain_count(h: int) -> int:
+    return h + h + 4 * h + 4 * h
+
+
+def wn_param_count(h: int, e: int) -> int:
+    return param_count(h, e) + wn_gain_count(h)
+
+
+def wn_split(flat: np.ndarray, h: int, e: int):
+    """Flat wn layout -> (dict of the 8 tensors with v in the W slots, dict of gains)."""
+    base = param_count(h, e)
+    P = unflatten(flat[:base], h, e)
+    gains, off = {}, base
+    for n in WN_NAMES:
+        rows = param_shapes(h, e)[n][0]
+        gains[n] = np.asarray(flat[off:off + rows], dtype=np.float64).copy()
+        off += rows
+    return P, gains
+
+
+def wn_join(P: dict, gains: dict) -> np.ndarray:
+    return np.concatenate([flatten(P)] + [np.asarray(gains[n], dtype=np.float64).ravel() for n in WN_NAMES])
+
+
+def weight_norm_build(v: np.ndarray, g: np.ndarray) -> np.ndarray:
+    """w_i = g_i * v_i / ||v_i||_2 per row (S:124 weight_norm_build; P:132 the norm in fp32 or wider)."""
+    v = np.asarray(v, dtype=np.float64)
+    norm = np.sqrt((v * v).sum(axis=1))
+    return (np.asarray(g, dtype=np.float64) / norm)[:, None] * v
+
+
+def weight_norm_backward(v: np.ndarray, g: np.ndarray, dw: np.ndarray):
+    """Chain rule through w = g v/||v||: dg_i = dw_i . v_i / ||v_i||,
+    dv_i = (g_i / ||v_i||) (dw_i - (dg_i / ||v_i||) v_i)   (Salimans & Kingma 2016, eq. 3)."""
+    v = np.asarray(v, dtype=np.float64)
+    dw = np.asarray(dw, dtype=np.float64)
+    norm = np.sqrt((v * v).sum(axis=1))
+    dg = (dw * v).sum(axis=1) / norm
+    dv = (np.asarray(g, dtype=np.float64) / norm)[:, None] * (dw - (dg / norm)[:, None] * v)
+    return dv, dg
+
+
+def wn_effective(P: dict, gains: dict) -> dict:
+    """The plain parameter dict the mLSTM runs with: W = weight_norm_build(v, g) for WN_NAMES."""
+    out = {n: np.asarray(P[n], dtype=np.float64).copy() for n in PARAM_NAMES}
+    for n in WN_NAMES:
+        out[n] = weight_norm_build(P[n], gains[n])
+    return out
+
+
+def wn_init(h: int, e: int, seed: int) -> np.ndarray:
+    """Flat wn parameters: v = the plain init (Q12), g_i = RNE_fp32(||v_i||) computed in fp64."""
+    P = init_params(h, e, seed)
+    gains = {n: np.sqrt((P[n] * P[n]).sum(axis=1)).astype(np.float32).astype(np.float64) for n in WN_NAMES}
+    return wn_join(P, gains)
+
+
+def wn_loss_and_grads(flat: np.ndarray, h: int, e: int, bytes_, h0, c0, n_global_rows=None, scale=1.0,
+                      reset=None):
+    """Forward + backward with weight normalisation; grads flat in the wn layout (dv, dg)."""
+    P, gains = wn_split(flat, h, e)
+    loss_sum, gw, state, cache = loss_and_grads(wn_effective(P, gains), bytes_, h0, c0, n_global_rows, scale,
+                                                reset=reset)
+    dg = {}
+    for n in WN_NAMES:
+        gw[n], dg[n] = weight_norm_backward(P[n], gains[n], gw[n])
+    return loss_sum, wn_join(gw, dg), state, cache
 
 
 # --------------------------------------------------------------------------------------
