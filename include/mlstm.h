@@ -17,6 +17,8 @@
  *  - Canonical parameter layout (flat, row-major, used by get/set_params, get_grads, opt state):
  *      E[256 x e] | W_mx[h x e] | W_mh[h x h] | W_x[4h x e] | W_h[4h x h] | b[4h] | W_dec[256 x h] | b_dec[256]
  *    with the 4h gate rows ordered i, f, o, u.  P = 5h^2 + 5he + 4h + 256e + 256h + 256.
+ *    With weight_norm = 1 the four W slots hold the directions v and the gains follow b_dec:
+ *      ... | b_dec[256] | g_mx[h] | g_mh[h] | g_x[4h] | g_h[4h]          (P grows by 10h, Q24)
  */
 #ifndef MLSTM_H_
 #define MLSTM_H_
@@ -57,7 +59,9 @@ typedef struct {
                            forward/backward per micro-batch and accumulates gradients in fp32
                            (P:130), then one allreduce + one update (4096 rows/GPU)    */
   int32_t precision;    /* MLSTM_MIXED (fp16 storage/multiply, fp32 accumulate) or MLSTM_FP32   */
-  int32_t weight_norm;  /* reserved, must be 0 (Q4)                                            */
+  int32_t weight_norm;  /* 0 or 1: weight normalisation of W_mx, W_mh, W_x, W_h (Q24):
+                           w_r = g_r v_r / ||v_r|| per output row; v in the W slots of the
+                           canonical layout, the 10h gains appended after b_dec; P grows by 10h  */
   uint64_t seed;        /* parameter init: counter-based SplitMix64, U(+-1/sqrt(cols)) (Q12)   */
   double lr0;           /* initial LR, 3e-3                                            */
   int64_t decay_iters;  /* linear decay to 0 over this many iterations, 100000         */

@@ -62,6 +62,66 @@ __device__ __forceinline__ void store_working(const Net<S>& n, long q, float val
   }
 }
 
+// ------------------------------------------------------------------ weight normalisation (Q24)
+// One warp per normalised row (W_mx, W_mh, W_x, W_h; w_r = g_r v_r / ||v_r||).
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// g_r = RNE_fp32(||v_r||) with the squared sum in fp64 (function-preserving init).
+__global__ void wn_init_gain_kernel(float* master, ParamOffsets po, int h, int e) {
+  const int lane = threadIdx.x & 31;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < 10 * h; r += (gridDim.x * blockDim.x) >> 5) {
+    long off, gi;
+    int len;
+    po.wn_row(h, e, r, off, len, gi);
+    double ss = 0.0;
+    for (int j = lane; j < len; j += 32) ss += (double)master[off + j] * master[off + j];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) master[gi] = __double2float_rn(sqrt(ss));
+  }
+}
+
+// ||v_r|| (fp32 squared sum; rounded to fp16 in mixed mode, "the final norm value is output
+// in FP16") and the effective weights g_r v_r / ||v_r|| into the working copies.
+template <typename S>
+__global__ void wn_norm_kernel(Net<S> n) {
+  const int lane = threadIdx.x & 31, h = n.h, e = n.e;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < 10 * h; r += (gridDim.x * blockDim.x) >> 5) {
+    long off, gi;
+    int len;
+    n.po.wn_row(h, e, r, off, len, gi);
+    float ss = 0.f;
+    for (int j = lane; j < len; j += 32) ss = fmaf(n.master[off + j], n.master[off + j], ss);
+    float nrm = sqrtf(warp_sum(ss));
+    if (sizeof(S) == 2) nrm = __half2float(__float2half_rn(nrm));
+    if (lane == 0) n.wn_norm[r] = nrm;
+    const float sc = n.master[gi] / nrm;
+    for (int j = lane; j < len; j += 32) store_working(n, off + j, n.master[off + j] * sc);
+  }
+}
+
+// After the allreduce: the gradient w.r.t. w in the arena becomes (dv, dg) in place
+// (dg_r = dw_r . v_r / ||v_r||, dv_r = (g_r / ||v_r||)(dw_r - (dg_r / ||v_r||) v_r)), alpha-scaled.
+template <typename S>
+__global__ void wn_grad_kernel(Net<S> n) {
+  const int lane = threadIdx.x & 31, h = n.h, e = n.e;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < 10 * h; r += (gridDim.x * blockDim.x) >> 5) {
+    long off, gi;
+    int len;
+    n.po.wn_row(h, e, r, off, len, gi);
+    float dot = 0.f;
+    for (int j = lane; j < len; j += 32) dot = fmaf(to_f(n.arena[off + j]), n.master[off + j], dot);
+    const float nrm = n.wn_norm[r];
+    const float dg = warp_sum(dot) / nrm, sc = n.master[gi] / nrm, k = dg / nrm;
+    for (int j = lane; j < len; j += 32) n.arena[off + j] = to_s<S>(sc * (to_f(n.arena[off + j]) - k * n.master[off + j]));
+    if (lane == 0) n.arena[gi] = to_s<S>(dg);
+  }
+}
+
 template <typename S>
 __global__ void cast_working_kernel(Net<S> n) {
   for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n.po.P; q += (long)gridDim.x * blockDim.x)
@@ -473,8 +533,11 @@ __global__ void adam_kernel(Net<S> n, float* __restrict__ m, float* __restrict__
     reinterpret_cast<float4*>(m)[q4] = mm;
     reinterpret_cast<float4*>(v)[q4] = vv;
     reinterpret_cast<float4*>(n.master)[q4] = th;
+    // normalised rows get their working copies from wn_norm_kernel once the whole row is updated
+    if (!(n.po.wn && q >= n.po.Wmx && q < n.po.b)) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) store_working(n, q + i, tp[i]);
+      for (int i = 0; i < 4; ++i) store_working(n, q + i, tp[i]);
+    }
   }
 }
 

@@ -281,6 +281,7 @@ void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
   n.hstate = cv.take<S>(2L * c->Bfull * h);
   n.cstate = cv.take<float>(2L * c->Bfull * h);
   n.gacc = c->nmb > 1 ? cv.take<float>(P) : nullptr;
+  n.wn_norm = c->po.wn ? cv.take<float>(10L * h) : nullptr;
   c->nblk_ce = (int)(((long)T * B + 31) / 32);
   n.loss_part = cv.take<double>(c->nblk_ce);
   n.colsum_part = cv.take<float>((long)c->nblk_ce * 256);
@@ -297,7 +298,7 @@ mlstm_status validate(const mlstm_config* cfg) {
   if (cfg->seq_len <= 0 || cfg->batch <= 0) return fail(MLSTM_EINVAL, "seq_len and batch must be positive");
   if (cfg->micro_batch < 0 || (cfg->micro_batch > 0 && cfg->batch % cfg->micro_batch != 0))
     return fail(MLSTM_EINVAL, "micro_batch must be 0 (= batch) or divide batch");
-  if (cfg->weight_norm != 0) return fail(MLSTM_EINVAL, "weight_norm must be 0 in this version (DESIGN Q4)");
+  if (cfg->weight_norm != 0 && cfg->weight_norm != 1) return fail(MLSTM_EINVAL, "weight_norm must be 0 or 1 (Q24)");
   if (cfg->precision != MLSTM_FP32 && cfg->precision != MLSTM_MIXED) return fail(MLSTM_EINVAL, "bad precision");
   if (!(cfg->decay_iters > 0) || !(cfg->lr0 >= 0)) return fail(MLSTM_EINVAL, "bad LR schedule");
   if (!(cfg->scale_min > 0) || !(cfg->scale_max >= cfg->scale_min) || !(cfg->scale_init >= cfg->scale_min) ||
@@ -316,7 +317,7 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   c->T = cfg->seq_len;
   c->Bp = c->B;
   c->Kt = (long)c->T * c->B;  // K of the weight-gradient GEMMs: every (t, b) of the micro-batch
-  c->po.set(c->h, c->e);
+  c->po.set(c->h, c->e, cfg->weight_norm);
   c->P = c->po.P;
   c->mixed = cfg->precision == MLSTM_MIXED;
   if (const char* v = getenv("MLSTM_L2_WMH")) c->l2_wmh = (float)atof(v);  // tuning knobs
@@ -610,6 +611,7 @@ template <typename S>
 mlstm_status enqueue_cast(mlstm_ctx* c) {
   Net<S>& n = net<S>(c);
   LAUNCH(c, (cast_working_kernel<S><<<grid_for(c->P), 256, 0, c->stream>>>(n)));
+  if (c->po.wn) LAUNCH(c, (wn_norm_kernel<S><<<grid_for(10L * c->h * 32), 256, 0, c->stream>>>(n)));
   return enqueue_transposes<S>(c);
 }
 
@@ -784,10 +786,12 @@ mlstm_status enqueue_train_b(mlstm_ctx* c) {
   Net<S>& n = net<S>(c);
   const mlstm_config& cf = c->cfg;
   phase(c, PH_OPT);
+  if (c->po.wn) LAUNCH(c, (wn_grad_kernel<S><<<grid_for(10L * c->h * 32), 256, 0, c->stream>>>(n)));
   LAUNCH(c, (overflow_kernel<S><<<grid_for(c->P), 256, 0, c->stream>>>(n.arena, c->P, &c->st->overflow)));
   LAUNCH(c, (adam_kernel<S><<<grid_for(c->P), 256, 0, c->stream>>>(n, c->adam_m, c->adam_v, (float)cf.beta1,
                                                                    (float)cf.beta2, (float)cf.eps, cf.lr0,
                                                                    (long)cf.decay_iters)));
+  if (c->po.wn) LAUNCH(c, (wn_norm_kernel<S><<<grid_for(10L * c->h * 32), 256, 0, c->stream>>>(n)));
   RET_IF(enqueue_transposes<S>(c));
   LAUNCH(c, (scaler_kernel<<<1, 1, 0, c->stream>>>(c->st, cf.scale_min, cf.scale_max, cf.scale_growth_interval,
                                                    cf.lr0, (long)cf.decay_iters)));
@@ -1017,7 +1021,7 @@ void mlstm_default_config(mlstm_config* cfg) {
 int64_t mlstm_param_count(const mlstm_config* cfg) {
   if (!cfg) return 0;
   ParamOffsets po;
-  po.set(cfg->hidden, cfg->embed);
+  po.set(cfg->hidden, cfg->embed, cfg->weight_norm);
   return po.P;
 }
 
@@ -1091,6 +1095,7 @@ mlstm_status mlstm_init(const mlstm_config* cfg, void* workspace, size_t workspa
     return bail(fail(MLSTM_ECUDA, "memcpy state"));
   float* master = c->mixed ? c->nh.master : c->nf.master;
   init_params_kernel<<<grid_for(c->P), 256, 0, c->stream>>>(master, c->po, c->h, c->e, cfg->seed);
+  if (c->po.wn) wn_init_gain_kernel<<<grid_for(10L * c->h * 32), 256, 0, c->stream>>>(master, c->po, c->h, c->e);
   if (cudaGetLastError() != cudaSuccess) return bail(fail(MLSTM_ECUDA, "init kernel"));
   mlstm_status s = c->mixed ? enqueue_cast<__half>(c) : enqueue_cast<float>(c);
   if (s != MLSTM_OK) return bail(s);

@@ -38,7 +38,9 @@ __host__ __device__ __forceinline__ int canon_of_int(int r, int h) {
 // Canonical flat parameter offsets (include/mlstm.h).
 struct ParamOffsets {
   long E, Wmx, Wmh, Wx, Wh, b, Wdec, bdec, P;
-  __host__ __device__ void set(int h, int e) {
+  long g;  // weight normalisation (Q24): gains g_mx[h] | g_mh[h] | g_x[4h] | g_h[4h] appended at `g`
+  int wn;  // weight normalisation on?
+  __host__ __device__ void set(int h, int e, int weight_norm = 0) {
     E = 0;
     Wmx = E + 256L * e;
     Wmh = Wmx + (long)h * e;
@@ -47,7 +49,17 @@ struct ParamOffsets {
     b = Wh + 4L * h * h;
     Wdec = b + 4L * h;
     bdec = Wdec + 256L * h;
-    P = bdec + 256;
+    g = bdec + 256;
+    wn = weight_norm;
+    P = g + (weight_norm ? 10L * h : 0);
+  }
+  // normalised row r in [0, 10h): its first element, length and gain index (canonical order)
+  __host__ __device__ void wn_row(int h, int e, int r, long& off, int& len, long& gi) const {
+    if (r < h) { off = Wmx + (long)r * e; len = e; }
+    else if (r < 2 * h) { off = Wmh + (long)(r - h) * h; len = h; }
+    else if (r < 6 * h) { off = Wx + (long)(r - 2 * h) * e; len = e; }
+    else { off = Wh + (long)(r - 6 * h) * h; len = h; }
+    gi = g + r;
   }
 };
 
@@ -99,6 +111,7 @@ struct Net {
   S* hstate;      // [2][Bfull][h]  persisted h per slot
   float* cstate;  // [2][Bfull][h]  persisted c per slot
   float* gacc;    // [P] fp32 gradient accumulator across micro-batches (nmb > 1)
+  float* wn_norm; // [10h] ||v_r|| of the normalised rows (fp32 sum; fp16-rounded in mixed mode)
   double* loss_part;
   float* colsum_part;
   DevState* st;

@@ -43,7 +43,7 @@ def test_workspace_size_and_validation():
     assert 0 < M.mlstm_workspace_bytes(small) < 64 << 20
     big = M.mlstm_default_config()
     assert 4e9 < M.mlstm_workspace_bytes(big) < 40e9          # fits a 180 GB B200 many times
-    for bad in [dict(hidden=100), dict(embed=48), dict(vocab=255), dict(weight_norm=1), dict(seq_len=0),
+    for bad in [dict(hidden=100), dict(embed=48), dict(vocab=255), dict(weight_norm=2), dict(seq_len=0),
                 dict(micro_batch=3), dict(precision=7), dict(scale_init=0.5)]:
         cfg = M.mlstm_default_config(**{**dict(hidden=64, seq_len=16, batch=4), **bad})
         with pytest.raises(M.MlstmError) as ei:
