@@ -195,6 +195,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--weight-norm", action="store_true",
+                    help="weight-normalised LSTM matrices (P:150; SURVEY NEXT #1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
@@ -213,8 +215,11 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     h, e, B, T, desc = CONFIGS[args.config]
+    if args.weight_norm:
+        desc += "; weight-normalised W_mx, W_mh, W_x, W_h (P:150)"
     cfg = M.mlstm_default_config(hidden=h, embed=e, batch=B, seq_len=T, precision=M.MLSTM_MIXED,
-                                 micro_batch=MICRO_BATCH.get(args.config, 0))
+                                 micro_batch=MICRO_BATCH.get(args.config, 0),
+                                 weight_norm=1 if args.weight_norm else 0)
     nid = None
     if world > 1:
         t = torch.zeros(128, dtype=torch.uint8, device="cuda")
