@@ -69,7 +69,7 @@ struct HasAsyncIO<E, decltype(void(E::kAsyncIO))> {
 
 template <int BN>
 struct TcCfg {  // one CTA per 128 x BN tile
-  static constexpr int BM = 128, BK = 64;
+  static constexpr int BM = 128, BK = 64, BNT = BN;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -79,11 +79,13 @@ struct TcCfg {  // one CTA per 128 x BN tile
 };
 template <int BN>
 struct Tc2Cfg {  // CTA pair per 256 x BN tile: per CTA 128 rows of A, BN/2 rows of B
-  static constexpr int BM = 128, BK = 64;
+  // BN = 512: two N = 256 MMAs per k-step into TMEM columns [0,256) and [256,512); each CTA holds
+  // the two 128-row B blocks of its rank ([r*128, +128) of each 256-wide half)
+  static constexpr int BM = 128, BK = 64, BNT = BN;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 6 : (BN == 128 ? 8 : 10);
+  static constexpr int STAGES = BN == 512 ? 4 : BN == 256 ? 6 : (BN == 128 ? 8 : 10);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512;
   static_assert(STAGES * STAGE_BYTES >= kEpiWarps * kWarpStageBytes, "epilogue staging windows");
 };
@@ -190,8 +192,18 @@ __device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUten
 #pragma unroll
       for (int i = 0; i < C::B_BYTES / 8192; ++i) {
         uint8_t* dst = L.sB + s * C::B_BYTES + i * 8192;
-        if (PAIR) ptx::tma_load_3d_2sm(dst, tmB, bar_leader0 + s * 8, nb0 + 64 * i, kb * C::BK, bz, pb);
-        else ptx::tma_load_3d(dst, tmB, &L.full[s], nb0 + 64 * i, kb * C::BK, bz, pb);
+        const int col = C::BNT == 512 ? nb0 + (i >> 1) * 256 + (i & 1) * 64 : nb0 + 64 * i;
+        if (PAIR) ptx::tma_load_3d_2sm(dst, tmB, bar_leader0 + s * 8, col, kb * C::BK, bz, pb);
+        else ptx::tma_load_3d(dst, tmB, &L.full[s], col, kb * C::BK, bz, pb);
+      }
+      return;
+    }
+    if constexpr (C::BNT == 512) {  // two 128-row boxes, N offsets 0 and 256 (no second segment)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        uint8_t* dst = L.sB + s * C::B_BYTES + i * 16384;
+        if (PAIR) ptx::tma_load_3d_2sm(dst, tmB, bar_leader0 + s * 8, kb * C::BK, nb0 + 256 * i, bz, pb);
+        else ptx::tma_load_3d(dst, tmB, &L.full[s], kb * C::BK, nb0 + 256 * i, bz, pb);
       }
       return;
     }
@@ -227,7 +239,8 @@ __device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUten
 template <class C, bool PAIR, int MMA_N, bool MN = false>
 __device__ __forceinline__ void gemm_mma(const SmemLayout<C>& L, uint32_t tmem, int nkb, uint16_t pair_mask,
                                          uint64_t* trace_slot) {
-  constexpr uint32_t idesc = ptx::idesc_f16_f32(PAIR ? 256 : 128, MMA_N, MN);
+  constexpr int MN_ = MMA_N > 256 ? 256 : MMA_N;  // BN = 512: two N = 256 MMAs per k-step
+  constexpr uint32_t idesc = ptx::idesc_f16_f32(PAIR ? 256 : 128, MN_, MN);
   constexpr int kstep = MN ? 2048 >> 4 : 32 >> 4;  // descriptor start-address step per K = 16
 #pragma unroll 1
   for (int i = 0; i < nkb; ++i) {
@@ -243,6 +256,11 @@ __device__ __forceinline__ void gemm_mma(const SmemLayout<C>& L, uint32_t tmem, 
     for (int k = 0; k < C::BK / 16; ++k) {
       if (PAIR) ptx::mma_f16_2sm(tmem, ad + kstep * k, bd + kstep * k, idesc, (i | k) != 0 ? 1u : 0u);
       else ptx::mma_f16(tmem, ad + kstep * k, bd + kstep * k, idesc, (i | k) != 0 ? 1u : 0u);
+      if constexpr (MMA_N == 512) {  // second half: B block at +16 KB, accumulator columns +256
+        const uint64_t bd2 = bd + (16384 >> 4);
+        if (PAIR) ptx::mma_f16_2sm(tmem + 256, ad + kstep * k, bd2 + kstep * k, idesc, (i | k) != 0 ? 1u : 0u);
+        else ptx::mma_f16(tmem + 256, ad + kstep * k, bd2 + kstep * k, idesc, (i | k) != 0 ? 1u : 0u);
+      }
     }
     if (PAIR) ptx::mma_commit_2sm_mc(&L.empty[s], pair_mask);
     else ptx::mma_commit(&L.empty[s]);
@@ -460,7 +478,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       if (nkb > 0)
-        gemm_produce<C, true, MN>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0 + rank * (BN / 2), az, bz, polA, polB, flags,
+        gemm_produce<C, true, MN>(L, &tmA, &tmB, &tmA2, &tmB2, sg, nkb, kb0, m0, n0 + rank * (BN == 512 ? 128 : BN / 2), az, bz, polA, polB, flags,
                               leader, ptx::mapa_shared(ptx::smem_u32(&L.full[0]), 0), MLSTM_TRACE_SLOT(1),
                               leader ? 2 : 0);
       l2_prefetch(pj);

@@ -109,6 +109,7 @@ struct mlstm_ctx {
   cudaEvent_t ev_wh = nullptr, ev_wmh = nullptr, ev_a_end = nullptr, ev_comm = nullptr;
   bool ar_overlap = true;
   int force_plan = 0;
+  bool wgrad512 = true;  // weight gradients on 256 x 512 pair tiles (MLSTM_WGRAD512=0: 256 x 256)
   int async_epi = 2;  // recurrent epilogue row I/O: 0 per-thread LSU, 1 bulk copies, 2 staged + coalesced (MLSTM_ASYNC_EPI)  // MLSTM_FORCE_PLAN (test instrument), applied while this ctx enqueues
   bool overlap_now() const { return world > 1 && ar_overlap && nmb == 1; }
   cudaGraphExec_t gA = nullptr, gB = nullptr;
@@ -328,6 +329,7 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   if (const char* v = getenv("MLSTM_L2_WH")) c->l2_wh = (float)atof(v);
   if (const char* v = getenv("MLSTM_AR_OVERLAP")) c->ar_overlap = v[0] != '0';
   if (const char* v = getenv("MLSTM_ASYNC_EPI")) c->async_epi = atoi(v);
+  if (const char* v = getenv("MLSTM_WGRAD512")) c->wgrad512 = v[0] != '0';
   {
     const char* v = getenv("MLSTM_FORCE_PLAN");
     const std::string fp = v ? v : "";
@@ -478,6 +480,10 @@ cudaError_t dispatch_tc(mlstm_ctx* c, const Plan& p, const CUtensorMap* ma, cons
                          : launch_tc1s<4, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, pj, epi);
   if (p.pair && p.persist && p.splits == 1)
     return launch_tc2p<256, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, pj, epi);
+  if constexpr (kMNEpi<Epi>) {
+    if (p.pair && p.bn == 512)
+      return launch_tc2<512, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
+  }
   if (p.pair) {
     if (MN || p.bn == 256)
       return launch_tc2<256, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
@@ -522,7 +528,8 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
   if constexpr (std::is_same<S, __half>::value) {
     if (c->tc) {
     const CUtensorMap* ma = get_map(c, A, 128);
-    const CUtensorMap* mb = get_map(c, B, p.pair ? p.bn / 2 : p.bn);
+    const int bbox = p.pair ? (p.bn == 512 ? 128 : p.bn / 2) : p.bn;  // B rows per TMA box (K-major)
+    const CUtensorMap* mb = get_map(c, B, bbox);
     if (!ma || !mb) {
       c->failed = MLSTM_ECUDA;
       return MLSTM_ECUDA;
@@ -531,7 +538,7 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
     const int gflags = B.weight ? (kGemmStaticB | kGemmRasterM) : 0;
     const PrefetchJob pj = pf.job;
     const CUtensorMap* ma2 = seg.A2 ? get_map(c, *seg.A2, 128) : ma;
-    const CUtensorMap* mb2 = seg.B2 ? get_map(c, *seg.B2, p.pair ? p.bn / 2 : p.bn) : mb;
+    const CUtensorMap* mb2 = seg.B2 ? get_map(c, *seg.B2, bbox) : mb;
     if (!ma2 || !mb2) {
       c->failed = MLSTM_ECUDA;
       return MLSTM_ECUDA;
@@ -750,7 +757,11 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
     };
     for (int wi = 0; wi < 4; ++wi) {
       const W& w = ws[wi];
-      const Plan p = plan_gemm(c->tc, w.M, w.N, Kt, true);
+      Plan p = plan_gemm(c->tc, w.M, w.N, Kt, true);
+      if (c->wgrad512 && p.pair && w.N % 512 == 0) {  // 256 x 512 pair tiles (MLSTM_WGRAD512)
+        p.bn = 512;
+        p.persist = false;
+      }
       if (p.splits == 1 || p.pair || p.cluster) {
         RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kt, p, EpiWgrad<S>{n, w.off, w.mode, (int)w.N}));
       } else {
@@ -1364,7 +1375,7 @@ int32_t mlstm_launches_per_step(mlstm_ctx* c) {
 
 mlstm_status mlstm_gemm_bench(int engine, int M, int N, int K, int bn, int iters, double* ms) {
   if (!ms || M <= 0 || N <= 0 || K <= 0 || iters <= 0 || engine < 1 || engine > 3 ||
-      (bn != 0 && bn != 64 && bn != 128 && bn != 256) || N % 64 || K % 8)
+      (bn != 0 && bn != 64 && bn != 128 && bn != 256 && !(bn == 512 && engine == 2)) || N % 64 || K % 8)
     return fail(MLSTM_EINVAL, "bad gemm_bench arguments");
   if (!get_encoder()) return fail(MLSTM_ECUDA, "cuTensorMapEncodeTiled unavailable");
   mlstm_ctx c;
@@ -1396,6 +1407,7 @@ mlstm_status mlstm_gemm_bench(int engine, int M, int N, int K, int bn, int iters
     p.pair = engine == 2;
     p.splits = 1;
     if (bn) p.bn = bn;
+    if (bn == 512) p.persist = false;
   }
   EpiPartial epi{D, N, (long)M * N};
   cudaEventCreate(&e0);

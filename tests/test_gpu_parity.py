@@ -252,12 +252,17 @@ def test_micro_batches_equal_one_batch(precision):
     assert rel_l2(split.get_params().astype(np.float64), whole.get_params().astype(np.float64)) < 1e-4
 
 
-@pytest.mark.parametrize("plan", ["pair", "split", "single", "persist"])
+@pytest.mark.parametrize("plan", ["pair", "split", "single", "persist", "pair512"])
 @pytest.mark.parametrize("h,B,T", [(512, 256, 4), (512, 200, 3), (1024, 256, 2)])
 def test_forced_tile_plans_match_oracle(plan, h, B, T, monkeypatch):
     """Every tcgen05 tile plan (CTA pair, cluster split-K, single CTA, persistent pairs) on every GEMM,
     forced at a size the oracle finishes quickly (full-size shapes select them on their own);
     B=200 leaves a ragged last M tile."""
+    if plan == "pair512":  # weight gradients on 256 x 512 pair tiles (two N=256 MMAs per k-step)
+        if h % 512:
+            pytest.skip("needs N % 512 == 0")
+        monkeypatch.setenv("MLSTM_WGRAD512", "1")
+        plan = "pair"
     monkeypatch.setenv("MLSTM_FORCE_PLAN", plan)
     if plan == "persist":  # two resident pairs: every pair walks several tiles (TMEM double buffer)
         monkeypatch.setenv("MLSTM_PERSIST_PAIRS", "2")
