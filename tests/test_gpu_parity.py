@@ -263,6 +263,8 @@ def test_forced_tile_plans_match_oracle(plan, h, B, T, monkeypatch):
             pytest.skip("needs N % 512 == 0")
         monkeypatch.setenv("MLSTM_WGRAD512", "1")
         plan = "pair"
+    else:
+        monkeypatch.setenv("MLSTM_WGRAD512", "0")
     monkeypatch.setenv("MLSTM_FORCE_PLAN", plan)
     if plan == "persist":  # two resident pairs: every pair walks several tiles (TMEM double buffer)
         monkeypatch.setenv("MLSTM_PERSIST_PAIRS", "2")
