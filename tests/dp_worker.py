@@ -15,6 +15,8 @@ from synth import bytestream  # noqa: E402
 
 def main():
     out, h, e, B, T, steps = sys.argv[1], *map(int, sys.argv[2:7])
+    micro = int(sys.argv[7]) if len(sys.argv) > 7 else 0
+    wn = int(sys.argv[8]) if len(sys.argv) > 8 else 0
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -22,7 +24,8 @@ def main():
     if rank == 0:
         t.copy_(torch.frombuffer(bytearray(M.mlstm_nccl_unique_id()), dtype=torch.uint8))
     dist.broadcast(t, 0)
-    cfg = M.mlstm_default_config(hidden=h, embed=e, batch=B, seq_len=T, precision=M.MLSTM_MIXED)
+    cfg = M.mlstm_default_config(hidden=h, embed=e, batch=B, seq_len=T, precision=M.MLSTM_MIXED,
+                                 micro_batch=micro, weight_norm=wn)
     m = M.MLSTM(cfg, rank=rank, world=world, nccl_id=bytes(t.cpu().numpy().tobytes()))
     theta0 = m.get_params()
     rows = np.arange(rank * B, (rank + 1) * B)

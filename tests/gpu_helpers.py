@@ -13,11 +13,20 @@ from synth import bytestream
 TOL = {"fp32": {"loss_rel": 1e-5, "grad_rel_l2": 1e-4}, "mixed": {"loss_rel": 5e-3, "grad_cos": 0.999}}
 
 
-def make_model(h, e, B, T, precision, seed=0x5EED, **kw):
+def oracle_theta(h, e, seed=0x5EED, weight_norm=False):
+    """The oracle's own initial parameters (flat, canonical): every parity test starts the GPU from
+    these (pushed through mlstm_set_params), so no oracle input is ever read back from the GPU."""
+    return O.wn_init(h, e, seed) if weight_norm else O.flatten(O.init_params(h, e, seed))
+
+
+def make_model(h, e, B, T, precision, seed=0x5EED, push_oracle=True, **kw):
     import paper_1808_01371_b200 as M
     cfg = M.mlstm_default_config(hidden=h, embed=e, seq_len=T, batch=B, seed=seed,
                                  precision=M.MLSTM_MIXED if precision == "mixed" else M.MLSTM_FP32, **kw)
-    return M.MLSTM(cfg)
+    m = M.MLSTM(cfg)
+    if push_oracle:
+        m.set_params(oracle_theta(h, e, seed, bool(kw.get("weight_norm", 0))))
+    return m
 
 
 def to_dev(a):

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 import torch
 
-from gpu_helpers import make_model, inputs, to_dev
+from gpu_helpers import make_model, inputs, oracle_theta, to_dev
 import oracle.mlstm_oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 def sampled_row_losses(h, e, B, T, micro, rows, precision="mixed"):
     m = make_model(h, e, B, T, precision, micro_batch=micro)
-    theta = m.get_params().astype(np.float64)
+    theta = oracle_theta(h, e)
     by = inputs(B, T)
     r = m.train_step(to_dev(by))
     mb = micro or B

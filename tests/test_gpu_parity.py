@@ -16,7 +16,7 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():
     pytest.skip("needs a B200", allow_module_level=True)
 
-from gpu_helpers import (TOL, compare_grads, inputs, make_model, oracle_step, rel_l2, split,  # noqa: E402
+from gpu_helpers import (TOL, oracle_theta, compare_grads, inputs, make_model, oracle_step, rel_l2, split,  # noqa: E402
                          to_dev)
 
 CASES = [
@@ -30,7 +30,7 @@ CASES = [
 @pytest.mark.parametrize("precision", ["fp32", "mixed"])
 def test_init_matches_oracle_bitwise(precision):
     h, e = 128, 64
-    m = make_model(h, e, 8, 4, precision, seed=1234)
+    m = make_model(h, e, 8, 4, precision, seed=1234, push_oracle=False)
     got = m.get_params()
     ref = O.flatten(O.init_params(h, e, 1234)).astype(np.float32)
     assert np.array_equal(got, ref)
@@ -40,7 +40,7 @@ def test_init_matches_oracle_bitwise(precision):
 @pytest.mark.parametrize("name,h,e,B,T", CASES)
 def test_train_step_parity(name, h, e, B, T, precision):
     m = make_model(h, e, B, T, precision)
-    theta0 = m.get_params().astype(np.float64)
+    theta0 = oracle_theta(h, e)
     by = inputs(B, T)
     res = m.train_step(to_dev(by))
     loss_ref, g_ref, (hT, cT), _ = oracle_step(theta0, by, h, e)
@@ -96,7 +96,7 @@ def test_byte_indexing_bit_exact(precision):
     m = make_model(h, e, B, T, precision)
     # a tiny W_dec (logit noise ~1e-5) and distinct b_dec make the 256 logits of every row distinct
     # by ~1e-2, so the target index of each per-position loss is identifiable from its value
-    P = split(m.get_params(), h, e)
+    P = split(oracle_theta(h, e), h, e)
     P["W_dec"] *= 1e-3
     P["b_dec"][:] = np.arange(256) * 1e-2
     m.set_params(O.flatten(P))
@@ -170,7 +170,7 @@ def test_loss_scale_overflow_decisions_and_replay():
 def test_eval_matches_oracle(precision):
     h, e, B, T = 128, 64, 16, 12
     m = make_model(h, e, B, T, precision)
-    P = split(m.get_params(), h, e)
+    P = split(oracle_theta(h, e), h, e)
     by = inputs(B, T, kind="markov")
     nats, tok, bpc = m.eval(to_dev(by))
     ref, tok_ref, _ = O.evaluate(P, by, np.zeros((B, h)), np.zeros((B, h)))
@@ -193,7 +193,7 @@ def test_state_carry_two_windows_bitwise():
         m.eval(to_dev(w2))
         outs.append(m.get_state(1))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
-    P = split(m.get_params(), h, e)
+    P = split(oracle_theta(h, e), h, e)
     _, _, (hT, cT) = O.forward(P, s, np.zeros((B, h)), np.zeros((B, h)))
     assert np.abs(outs[0][0] - hT).max() < 1e-5
 
@@ -206,7 +206,7 @@ def test_reset_rows_start_from_zero_state():
     m.set_state(h0, c0)
     by = inputs(B, T)
     reset = np.array([0, 1, 0, 1], dtype=np.uint8)
-    theta0 = m.get_params().astype(np.float64)
+    theta0 = oracle_theta(h, e)
     r = m.train_step(to_dev(by), to_dev(reset))
     h0r, c0r = h0.astype(np.float64), c0.astype(np.float64)
     h0r[reset == 1] = 0
@@ -270,7 +270,7 @@ def test_forced_tile_plans_match_oracle(plan, h, B, T, monkeypatch):
         monkeypatch.setenv("MLSTM_PERSIST_PAIRS", "2")
     e = 64
     m = make_model(h, e, B, T, "mixed")
-    theta0 = m.get_params().astype(np.float64)
+    theta0 = oracle_theta(h, e)
     by = inputs(B, T)
     res = m.train_step(to_dev(by))
     loss_ref, g_ref, (hT, cT), _ = oracle_step(theta0, by, h, e)
