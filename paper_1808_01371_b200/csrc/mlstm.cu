@@ -19,6 +19,7 @@
 #include "../../include/mlstm.h"
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "bwd_persist.cuh"
 
 using namespace mlstm;
 
@@ -109,7 +110,9 @@ struct mlstm_ctx {
   cudaEvent_t ev_wh = nullptr, ev_wmh = nullptr, ev_a_end = nullptr, ev_comm = nullptr;
   bool ar_overlap = true;
   int force_plan = 0;
-  bool wgrad512 = true;  // weight gradients on 256 x 512 pair tiles (MLSTM_WGRAD512=0: 256 x 256)
+  bool wgrad512 = true;
+  bool bwd_persist = false;    // backward recurrence as one persistent kernel (MLSTM_BWD_PERSIST=1; measured slower)
+  uint32_t* bwd_sync = nullptr;  // weight gradients on 256 x 512 pair tiles (MLSTM_WGRAD512=0: 256 x 256)
   int async_epi = 2;  // recurrent epilogue row I/O: 0 per-thread LSU, 1 bulk copies, 2 staged + coalesced (MLSTM_ASYNC_EPI)  // MLSTM_FORCE_PLAN (test instrument), applied while this ctx enqueues
   bool overlap_now() const { return world > 1 && ar_overlap && nmb == 1; }
   cudaGraphExec_t gA = nullptr, gB = nullptr;
@@ -278,6 +281,7 @@ void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
   c->part_elems = part;
   n.part = cv.take<float>(part);
   c->split_scratch = c->tc ? cv.take<float>(kSplitScratchFloats) : nullptr;
+  c->bwd_sync = cv.take<uint32_t>(kBwdSyncWords + 256);
   n.Scan = cv.take<float>(256L * 5 * h);
   n.hstate = cv.take<S>(2L * c->Bfull * h);
   n.cstate = cv.take<float>(2L * c->Bfull * h);
@@ -330,6 +334,7 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   if (const char* v = getenv("MLSTM_AR_OVERLAP")) c->ar_overlap = v[0] != '0';
   if (const char* v = getenv("MLSTM_ASYNC_EPI")) c->async_epi = atoi(v);
   if (const char* v = getenv("MLSTM_WGRAD512")) c->wgrad512 = v[0] != '0';
+  if (const char* v = getenv("MLSTM_BWD_PERSIST")) c->bwd_persist = v[0] != '0';
   {
     const char* v = getenv("MLSTM_FORCE_PLAN");
     const std::string fp = v ? v : "";
@@ -678,6 +683,74 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   return MLSTM_OK;
 }
 
+// The persistent backward kernel applies when both per-step GEMMs take the S = 4 split-K cluster
+// plan with one resident wave (C2, C3) on the tcgen05 path; the cooperative launch guarantees
+// co-residency of the grid (it fails rather than deadlocks otherwise).
+bool bwd_persist_ok(mlstm_ctx* c) {
+  if (!c->bwd_persist || !c->tc || !c->mixed || g_force_plan != 0 || c->h % 256) return false;
+  const Plan p1 = plan_gemm(true, c->B, c->h, 4L * c->h, false), p2 = plan_gemm(true, c->B, c->h, c->h, false);
+  if (!p1.cluster || !p2.cluster || p1.splits != 4 || p2.splits != 4) return false;
+  const long ctas = 4L * (c->h / 256) * ((c->B + 127) / 128);
+  if (ctas > 148 || (ctas / 4) * 4 * 128L * 256 > kSplitScratchFloats || ctas / 4 > 256) return false;
+  static int max_clusters = -1;
+  if (max_clusters < 0) {
+    cudaFuncSetAttribute(bwd_persist_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<256>::SMEM);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(4, 1, 1);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = TcCfg<256>::SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 4;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int mc = 0;
+    max_clusters = cudaOccupancyMaxActiveClusters(&mc, bwd_persist_kernel<4>, &cfg) == cudaSuccess ? mc : 0;
+    cudaGetLastError();
+  }
+  return ctas / 4 <= max_clusters;
+}
+
+mlstm_status launch_bwd_persist(mlstm_ctx* c) {
+  Net<__half>& n = c->nh;
+  const int h = c->h, B = c->B, T = c->T;
+  const Opd dZ{n.G5 + h, B, 4L * h, 5L * h, T, 5L * B * h, kPolFirst};
+  const Opd WhT{n.WhT, h, 4L * h, 4L * h, 1, 4L * h * h, 0, true};
+  const Opd dA{n.dA, B, h, h, T, (long)B * h, kPolFirst};
+  const Opd WmhT{n.WmhT, h, h, h, 1, (long)h * h, 0, true};
+  const Opd dYs{n.dY, B, 256, 256, T, (long)B * 256, kPolFirst};
+  const Opd WdecT{n.WdecT, h, 256, 256, 1, 256L * h, 0, true};
+  const CUtensorMap *a1 = get_map(c, dZ, 128), *b1 = get_map(c, WhT, 256), *a2 = get_map(c, dA, 128),
+                    *b2 = get_map(c, WmhT, 256), *a2s = get_map(c, dYs, 128), *b2s = get_map(c, WdecT, 256);
+  if (!a1 || !b1 || !a2 || !b2 || !a2s || !b2s) {
+    c->failed = MLSTM_ECUDA;
+    return MLSTM_ECUDA;
+  }
+  CUDA_OR_FAIL(c, cudaMemsetAsync(c->bwd_sync, 0, sizeof(uint32_t) * (kBwdSyncWords + 256), c->stream));
+  CUDA_OR_FAIL(c, cudaFuncSetAttribute(bwd_persist_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       TcCfg<256>::SMEM));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(4 * (h / 256), (B + 127) / 128, 1);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = TcCfg<256>::SMEM;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 4;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  CUDA_OR_FAIL(c, cudaLaunchKernelEx(&cfg, bwd_persist_kernel<4>, *a1, *b1, *a2, *b2, *a2s, *b2s, n,
+                                     c->split_scratch, c->bwd_sync));
+  count_launch(c);
+  return MLSTM_OK;
+}
+
 template <typename S>
 mlstm_status enqueue_train_a(mlstm_ctx* c) {
   Net<S>& n = net<S>(c);
@@ -719,7 +792,9 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
     const Plan p1 = plan_gemm(c->tc, B, h, 4 * h, false), p2 = plan_gemm(c->tc, B, h, h, false);
     // B2 prefetches into L2 the first k-blocks (of each K split) of the W_h^T tiles B1 streams next
     const size_t es = sizeof(S);
-    for (int t = T - 1; t >= 0; --t) {
+    const bool persist = std::is_same<S, __half>::value && bwd_persist_ok(c);
+    if (persist) RET_IF(launch_bwd_persist(c));
+    for (int t = persist ? -1 : T - 1; t >= 0; --t) {
       // B1(t) prefetches what B2's gate backward of step t-1 reads (written long ago by the
       // forward: gates, c_{t-1} and c_{t-2} (adjacent blocks), dH_dec); B2 prefetches the a-stash
       // block the next B1 reads.

@@ -281,3 +281,19 @@ def test_forced_tile_plans_match_oracle(plan, h, B, T, monkeypatch):
     assert np.abs(hs - hT).max() <= 2e-3 and np.abs(cs - cT).max() <= 2e-2
     nats, tokens, _ = m.eval(to_dev(inputs(B, T, k=1)))
     assert np.isfinite(nats) and tokens == B * T
+
+
+@pytest.mark.parametrize("h,B,T", [(1024, 128, 6), (1024, 200, 3)])
+def test_persistent_backward_matches_oracle(h, B, T, monkeypatch):
+    """The backward recurrence as one persistent cooperative kernel (MLSTM_BWD_PERSIST=1: grid-wide
+    phase barriers, split-K counters in global memory) against the oracle; B=200 is ragged."""
+    monkeypatch.setenv("MLSTM_BWD_PERSIST", "1")
+    e = 64
+    m = make_model(h, e, B, T, "mixed")
+    theta0 = oracle_theta(h, e)
+    by = inputs(B, T)
+    res = m.train_step(to_dev(by))
+    loss_ref, g_ref, (hT, cT), _ = oracle_step(theta0, by, h, e)
+    assert abs(res["loss_nats"] - loss_ref) / loss_ref <= TOL["mixed"]["loss_rel"]
+    rep = compare_grads(m.get_grads().astype(np.float64), g_ref, h, e, "mixed")
+    assert min(rep.values()) >= TOL["mixed"]["grad_cos"], rep
