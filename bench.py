@@ -55,10 +55,10 @@ def phase_flops(h, e, B, T):
     BT = B * T
     return {
         "fwd_rec": 2.0 * BT * 5 * h * h,                                   # W_mh h, W_h m per char
-        "bwd_rec": 2.0 * BT * 5 * h * h - 2.0 * B * h * h,                 # dZ W_h, dA W_mh (t>0)
+        "bwd_rec": 2.0 * BT * 5 * h * h - 2.0 * B * h * h + 2.0 * BT * 256 * h,  # dZ W_h, dA W_mh (t>0),
+                                                                            # dY W_dec (folded into B2)
         "wgrad": 2.0 * BT * (5 * h * h + 5 * h * e + 256 * h),             # dW_h, dW_mh, dW_x, dW_mx, dW_dec
         "decoder": 2.0 * BT * 256 * h,
-        "dhdec": 2.0 * BT * 256 * h,
     }
 
 
@@ -308,6 +308,11 @@ def main():
             "kernel": f"gemm_tc_kernel ({dom} phase: {dom_launches} launches/step, "
                       f"{pf[dom] / dom_launches / 1e9:.2f} GFLOP per launch avg, "
                       f"{dom_ms / dom_launches * 1e3:.1f} us per launch avg)"}
+    # every GEMM phase against the same sustained peak (the weight-gradient phase is the one that
+    # reaches the tensor roofline; the recurrence is bound by per-timestep latency + weight streaming)
+    roof_phases = {k: {"tflops": round(pf[k] / (gem[k][0] / args.steps / 1e3) / 1e12, 1),
+                       "frac": round(pf[k] / (gem[k][0] / args.steps / 1e3) / 1e12 / sustained, 3),
+                       "ms": round(gem[k][0] / args.steps, 3)} for k in gem if gem[k][0] > 0}
     whole = flops_per_char(h, e) * world * B * T / (ms_step / 1e3) / 1e12 / world
     line = {
         "metric": METRIC, "value": value, "unit": "chars/s", "n_gpus": world, "steps": args.steps,
@@ -315,7 +320,7 @@ def main():
         "vs_baseline": None, "dtype": "f16 (fp32 accumulate, fp32 masters)", "data": "synthetic",
         "config": {"workload": desc, "global_batch": world * B, "seq_len": T, "parallelism": f"dp{world}",
                    "l2": "no flush: per-step working set (~11 GB) >> 126 MB L2"},
-        "roofline": roof,
+        "roofline": roof, "roofline_phases": roof_phases,
         "step_tflops_per_gpu": whole, "step_frac_of_sustained_peak": whole / sustained,
         "phases_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in phases.items()},
         "clocks": clk, "e2e": e2e, "gpu_launches": launches * args.steps,
