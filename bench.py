@@ -50,6 +50,14 @@ def flops_per_char(h, e):
     return 6.0 * (5 * h * h + 5 * h * e + 256 * h)
 
 
+PHASE_KERNELS = {  # what each GEMM phase launches at C3 (profiles/r01_launch_summary_final.txt)
+    "bwd_rec": "gemm_tc1s_kernel<4,EpiB1IO> + gemm_tc1s_kernel<4,EpiB2> per timestep",
+    "fwd_rec": "gemm_tc1s_kernel<4,EpiF1IO> + gemm_tc2_kernel<256,EpiF2IO> per timestep",
+    "wgrad": "gemm_tc2_kernel<512,EpiWgrad,MN> (dW_h, dW_mh, dW_dec) + per-byte sums",
+    "decoder": "gemm_tc2p_kernel<256,EpiY>",
+}
+
+
 def phase_flops(h, e, B, T):
     """Algorithmic FLOPs of each GEMM phase of one step (per rank)."""
     BT = B * T
@@ -305,7 +313,7 @@ def main():
     roof = {"bound": "tensor", "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
             "frac": achieved / sustained, "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
             "peak_source": f"{src} bf16_tflops_sustained",
-            "kernel": f"gemm_tc_kernel ({dom} phase: {dom_launches} launches/step, "
+            "kernel": f"{PHASE_KERNELS.get(dom, 'tcgen05 GEMMs')} ({dom} phase: {dom_launches} launches/step, "
                       f"{pf[dom] / dom_launches / 1e9:.2f} GFLOP per launch avg, "
                       f"{dom_ms / dom_launches * 1e3:.1f} us per launch avg)"}
     # every GEMM phase against the same sustained peak (the weight-gradient phase is the one that
