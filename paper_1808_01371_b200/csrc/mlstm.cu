@@ -1559,3 +1559,5 @@ void mlstm_destroy(mlstm_ctx* c) {
 }
 
 }  // extern "C"
+
+#include "loader.cuh"

@@ -9,6 +9,7 @@ passes torch's current stream (PyTorch is used for memory, streams and process g
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import re
 
@@ -17,6 +18,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MLSTM_LIB") or os.path.join(HERE, "libmlstm.so")  # MLSTM_LIB: A/B experiments
 HEADER = os.path.join(os.path.dirname(HERE), "include", "mlstm.h")
+HEADERS = [HEADER, os.path.join(os.path.dirname(HERE), "include", "mlstm_data.h")]
 
 MLSTM_OK, MLSTM_EINVAL, MLSTM_ECUDA, MLSTM_ENCCL, MLSTM_ENOMEM, MLSTM_ESTATE, MLSTM_EDIVERGED = range(7)
 MLSTM_FP32, MLSTM_MIXED = 0, 1
@@ -92,6 +94,18 @@ _SIGS = {
                                          ctypes.c_int, _dp]),
     "mlstm_trace_enable": (ctypes.c_int, [ctypes.c_int]),
     "mlstm_trace_read": (ctypes.c_int, [_P(ctypes.c_uint64), ctypes.c_int, _i32p]),
+    # data pipeline (include/mlstm_data.h)
+    "mlstm_corpus_create": (ctypes.c_int, [_u8p, _P(ctypes.c_int64), ctypes.c_int64, ctypes.c_uint64,
+                                           _P(ctypes.c_void_p)]),
+    "mlstm_corpus_split_sizes": (ctypes.c_int, [_vp, _P(ctypes.c_int64)]),
+    "mlstm_corpus_destroy": (None, [_vp]),
+    "mlstm_loader_create": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.c_uint64, _P(ctypes.c_void_p)]),
+    "mlstm_loader_num_shards": (ctypes.c_int64, [_vp]),
+    "mlstm_loader_shard": (ctypes.c_int, [_vp, ctypes.c_int64, _u8p, ctypes.c_int64, _P(ctypes.c_int64)]),
+    "mlstm_loader_next": (ctypes.c_int, [_vp, _u8p, _u8p, _i32p]),
+    "mlstm_loader_rewind": (ctypes.c_int, [_vp]),
+    "mlstm_loader_destroy": (None, [_vp]),
     "mlstm_last_error": (ctypes.c_char_p, []),
     "mlstm_destroy": (None, [_vp]),
 }
@@ -113,10 +127,12 @@ def lib():
 
 
 def header_functions():
-    """Names of the functions include/mlstm.h declares."""
-    src = open(HEADER).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(mlstm_[a-z_0-9]+)\s*\(", src)))
+    """Names of the functions include/*.h declare (mlstm.h: the step; mlstm_data.h: the data pipeline)."""
+    names = set()
+    for h in HEADERS:
+        src = re.sub(r"/\*.*?\*/", "", open(h).read(), flags=re.S)
+        names |= set(re.findall(r"\b(mlstm_[a-z_0-9]+)\s*\(", src))
+    return sorted(names)
 
 
 def _check(status):
@@ -339,3 +355,95 @@ class MLSTM:
         if n < 0:
             _check(MLSTM_ECUDA)
         return int(n)
+
+
+# ------------------------------------------------------------------ data pipeline (mlstm_data.h)
+MLSTM_SPLIT_TRAIN, MLSTM_SPLIT_VAL, MLSTM_SPLIT_TEST = 0, 1, 2
+MLSTM_SHARDS_TRAIN, MLSTM_SHARDS_EVAL = 0, 1
+
+
+class Corpus:
+    """Records (list of bytes) -> the 1000:1:1 split held by the library."""
+
+    def __init__(self, records, seed: int = 0x5EED):
+        self.h = None
+        data = np.frombuffer(b"".join(records), dtype=np.uint8) if records else np.zeros(0, np.uint8)
+        data = np.ascontiguousarray(data) if data.size else np.zeros(1, np.uint8)
+        offs = np.zeros(len(records) + 1, dtype=np.int64)
+        offs[1:] = np.cumsum([len(r) for r in records])
+        h = ctypes.c_void_p()
+        _check(lib().mlstm_corpus_create(_ptr(data, ctypes.c_uint8), offs.ctypes.data_as(_P(ctypes.c_int64)), len(records),
+                                         seed, ctypes.byref(h)))
+        self.h = h
+
+    def split_sizes(self):
+        out = (ctypes.c_int64 * 3)()
+        _check(lib().mlstm_corpus_split_sizes(self.h, out))
+        return tuple(out)
+
+    def close(self):
+        if self.h:
+            lib().mlstm_corpus_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+
+class Loader:
+    """Shard-contiguous TBTT minibatches of one split: next() -> (bytes [B][T+1], reset [B])
+    or None at the end of the epoch."""
+
+    def __init__(self, corpus: Corpus, split: int, kind: int, B: int, T: int, seed: int = 0x5EED):
+        self.h = None
+        h = ctypes.c_void_p()
+        _check(lib().mlstm_loader_create(corpus.h, split, kind, B, T, seed, ctypes.byref(h)))
+        self.h, self.B, self.T = h, B, T
+
+    def num_shards(self) -> int:
+        return lib().mlstm_loader_num_shards(self.h)
+
+    def shard(self, i: int) -> bytes:
+        n = ctypes.c_int64()
+        _check(lib().mlstm_loader_shard(self.h, i, None, 0, ctypes.byref(n)))
+        buf = np.zeros(max(1, n.value), dtype=np.uint8)
+        _check(lib().mlstm_loader_shard(self.h, i, _ptr(buf, ctypes.c_uint8), n.value, ctypes.byref(n)))
+        return buf[:n.value].tobytes()
+
+    def next(self):
+        by = np.zeros((self.B, self.T + 1), dtype=np.uint8)
+        rs = np.zeros(self.B, dtype=np.uint8)
+        end = ctypes.c_int32()
+        _check(lib().mlstm_loader_next(self.h, _ptr(by, ctypes.c_uint8), _ptr(rs, ctypes.c_uint8), ctypes.byref(end)))
+        return None if end.value else (by, rs)
+
+    def rewind(self):
+        _check(lib().mlstm_loader_rewind(self.h))
+
+    def __iter__(self):
+        while True:
+            b = self.next()
+            if b is None:
+                return
+            yield b
+
+    def close(self):
+        if self.h:
+            lib().mlstm_loader_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+
+def heldout_bpc(model, loader: Loader, max_batches: int | None = None) -> float:
+    """Held-out BPC over one epoch of an evaluation loader: every window through mlstm_eval
+    with the loader's reset masks (state persisted within a shard, zero at a shard start)."""
+    import torch
+    nats = tokens = 0
+    loader.rewind()
+    for k, (by, rs) in enumerate(loader):
+        if max_batches is not None and k >= max_batches:
+            break
+        n, tok, _ = model.eval(torch.from_numpy(by).cuda(), torch.from_numpy(rs).cuda())
+        nats += n
+        tokens += tok
+    return nats / tokens / math.log(2.0)
