@@ -447,3 +447,21 @@ def heldout_bpc(model, loader: Loader, max_batches: int | None = None) -> float:
         nats += n
         tokens += tok
     return nats / tokens / math.log(2.0)
+
+
+def cell_features(model, texts):
+    """Frozen-feature transfer: the final cell state c_T of each text after a
+    forward-only pass from a zero state (mlstm_eval over consecutive T-byte windows with the state
+    carried, reset at the first window).  texts: list of equal-length byte strings of
+    1 + k*T bytes, at most `batch` of them per call.  Returns float32 [len(texts), h]."""
+    import torch
+    n, T = len(texts), model.T
+    L = len(texts[0])
+    if n > model.B or any(len(t) != L for t in texts) or (L - 1) % T or L < T + 1:
+        raise ValueError("texts: <= batch strings of equal length 1 + k*T")
+    arr = np.frombuffer(b"".join(texts), dtype=np.uint8).reshape(n, L)
+    reset = torch.ones(n, dtype=torch.uint8, device="cuda")
+    for k in range((L - 1) // T):
+        window = torch.from_numpy(np.ascontiguousarray(arr[:, k * T: k * T + T + 1])).cuda()
+        model.eval(window, reset if k == 0 else None)
+    return model.get_state(MLSTM_SLOT_EVAL)[1][:n].copy()
