@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // the reduction phase's rows/columns of this thread (tid mapping below); loads land in the
       // idle stages while the partials are exchanged
       const int tid = threadIdx.x - 64, hh = tid >> 7;
-      const EpiIO io = L.io(warp - 2, m0 + (tid & 127) - lane, M, lane);
+      const EpiIO io = L.io(warp - 2, m0 + q * 32, M, lane);
       if (HALF_ROWS || hh == 0)
         for (int j = 0; j < WIDTH / PIECE; ++j) {
           const int col0 = n0 + z * SLICE + (HALF_ROWS ? hh * WIDTH : 0) + j * PIECE;
@@ -755,6 +755,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     float4* dst = reinterpret_cast<float4*>(part + (long)z * 128 * BN) + rl;
 #pragma unroll 1
     for (int c = grp; c < BN / 64; c += 2) {
+      if (c * 64 >= z * SLICE && c * 64 < (z + 1) * SLICE) continue;  // own slice: re-read from TMEM
       float v[64];
       tmem_chunk(tmem, q, c, nkb > 0, v);
 #pragma unroll
@@ -767,7 +768,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (tracing && threadIdx.x == 0) tr_ts[4] = ptx::globaltimer();
   if (warp >= 2) {
     const int tid = threadIdx.x - 64;
-    const int rl = tid & 127, hh = tid >> 7;
+    const int q = warp & 3, rl = q * 32 + lane, hh = tid >> 7;  // TMEM lane quarter of this warp
     const int row = m0 + rl;
     if (HALF_ROWS || hh == 0) {
 #pragma unroll 1
@@ -778,6 +779,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int i = 0; i < PIECE; ++i) v[i] = 0.f;
 #pragma unroll 1
         for (int zz = 0; zz < S; ++zz) {
+          if (zz == z) {  // this CTA's own partial is still in TMEM
+            if (nkb > 0) {
+              float o[PIECE];
+              const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + cl;
+#pragma unroll
+              for (int i = 0; i < PIECE / 16; ++i) ptx::tmem_ld16(ta + 16 * i, o + 16 * i);
+              ptx::tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < PIECE; ++i) v[i] += o[i];
+            }
+            continue;
+          }
           const float4* src = reinterpret_cast<const float4*>(part + (long)zz * 128 * BN) + (cl / 4) * 128 + rl;
 #pragma unroll
           for (int i = 0; i < PIECE / 4; ++i) {
