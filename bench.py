@@ -1,7 +1,7 @@
 """Benchmark: training chars/s of the paper's 4096-d mLSTM step (seq 256, 256 rows/GPU, mixed fp16/fp32
 with dynamic loss scaling) on N B200s, data parallel (BASELINE.json `metric`, configs[2]).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3|C1|C2|C5]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C1|C2|C3|C4|C5] [--weight-norm]
   N > 1: python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
 
 Rank 0 prints ONE JSON line.  `value` = N*B*T / (max over ranks of the CUDA-event time of K steps)/K,
