@@ -109,11 +109,11 @@ struct mlstm_ctx {
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_wh = nullptr, ev_wmh = nullptr, ev_a_end = nullptr, ev_comm = nullptr;
   bool ar_overlap = true;
-  int force_plan = 0;
-  bool wgrad512 = true;
+  int force_plan = 0;          // MLSTM_FORCE_PLAN (test instrument), applied while this ctx enqueues
+  bool wgrad512 = true;        // weight gradients on 256 x 512 pair tiles (MLSTM_WGRAD512=0: 256 x 256)
   bool bwd_persist = false;    // backward recurrence as one persistent kernel (MLSTM_BWD_PERSIST=1; measured slower)
-  uint32_t* bwd_sync = nullptr;  // weight gradients on 256 x 512 pair tiles (MLSTM_WGRAD512=0: 256 x 256)
-  int async_epi = 2;  // recurrent epilogue row I/O: 0 per-thread LSU, 1 bulk copies, 2 staged + coalesced (MLSTM_ASYNC_EPI)  // MLSTM_FORCE_PLAN (test instrument), applied while this ctx enqueues
+  uint32_t* bwd_sync = nullptr;  // its grid / split-K counters
+  int async_epi = 2;  // recurrent epilogue row I/O: 0 per-thread LSU, 1 bulk copies, 2 staged + coalesced (MLSTM_ASYNC_EPI)
   bool overlap_now() const { return world > 1 && ar_overlap && nmb == 1; }
   cudaGraphExec_t gA = nullptr, gB = nullptr;
   std::map<std::tuple<const void*, long, long, long, long, long, int>, CUtensorMap> maps;
