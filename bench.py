@@ -321,6 +321,15 @@ def main():
     roof_phases = {k: {"tflops": round(pf[k] / (gem[k][0] / args.steps / 1e3) / 1e12, 1),
                        "frac": round(pf[k] / (gem[k][0] / args.steps / 1e3) / 1e12 / sustained, 3),
                        "ms": round(gem[k][0] / args.steps, 3)} for k in gem if gem[k][0] > 0}
+    # the recurrences also against HBM: every timestep re-streams the recurrent weights (fp16) and
+    # moves its stash rows (10h^2 weight bytes per timestep and direction-pair; ~48h
+    # stash bytes per row per timestep over both directions)
+    for k, wbytes in (("fwd_rec", 2.0 * 5 * h * h), ("bwd_rec", 2.0 * (5 * h * h + 256 * h))):
+        if k in roof_phases:
+            byts = T * (wbytes + 24.0 * h * B)
+            gbs = byts / (gem[k][0] / args.steps / 1e3) / 1e9
+            roof_phases[k]["hbm_gbs"] = round(gbs, 1)
+            roof_phases[k]["hbm_frac"] = round(gbs / hbm, 3)
     whole = flops_per_char(h, e) * world * B * T / (ms_step / 1e3) / 1e12 / world
     line = {
         "metric": METRIC, "value": value, "unit": "chars/s", "n_gpus": world, "steps": args.steps,
