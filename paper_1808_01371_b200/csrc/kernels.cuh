@@ -122,6 +122,31 @@ __global__ void wn_grad_kernel(Net<S> n) {
   }
 }
 
+// Four consecutive parameters q..q+3 (never straddling a tensor or a row: P, e, h are multiples of
+// 64) into the working copies with one vector store; 32-bit index arithmetic within a tensor.
+template <typename S>
+__device__ __forceinline__ void store_working4(const Net<S>& n, long q, const float* val) {
+  const ParamOffsets& po = n.po;
+  const int h = n.h, e = n.e;
+  S* dst = nullptr;
+  if (q < po.Wmx) {
+    dst = n.E_w + q;
+  } else if (q < po.Wmh) {
+    dst = n.Wcat_w + (q - po.Wmx);
+  } else if (q < po.Wx) {
+    dst = n.Wmh_w + (q - po.Wmh);
+  } else if (q < po.Wh) {
+    const unsigned o = (unsigned)(q - po.Wx), r = o / (unsigned)e, c = o - r * (unsigned)e;
+    dst = n.Wcat_w + ((long)h + int_row((int)(r / h), (int)(r % h))) * e + c;
+  } else if (q < po.b) {
+    const unsigned o = (unsigned)(q - po.Wh), r = o / (unsigned)h, c = o - r * (unsigned)h;
+    dst = n.Wh_w + (long)int_row((int)(r / h), (int)(r % h)) * h + c;
+  } else if (q >= po.Wdec && q < po.bdec) {
+    dst = n.Wdec_w + (q - po.Wdec);
+  }
+  if (dst) st4(dst, make_float4(val[0], val[1], val[2], val[3]));
+}
+
 template <typename S>
 __global__ void cast_working_kernel(Net<S> n) {
   for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n.po.P; q += (long)gridDim.x * blockDim.x)
@@ -293,24 +318,28 @@ __global__ void __launch_bounds__(256) ce_kernel(Net<S> n, int Be, float inv_den
   }
 }
 
-// Final fixed-order reductions of the CE partials: local loss sum -> st->loss_sum; db_dec.
+// Final fixed-order reductions of the CE partials: block 0 sums the loss partials into
+// st->loss_sum; with_grad: block 1 + v sums column v of the db_dec partials (strided per thread,
+// then a fixed-shape tree: deterministic).  Grid = 1 + 256 * with_grad blocks of 256 threads.
 template <typename S>
 __global__ void __launch_bounds__(256) ce_reduce_kernel(Net<S> n, int nblk, int with_grad) {
   __shared__ double red[256];
   double s = 0.0;
-  for (int i = threadIdx.x; i < nblk; i += 256) s += n.loss_part[i];
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < nblk; i += 256) s += n.loss_part[i];
+  } else {
+    const int v = blockIdx.x - 1;
+    for (int i = threadIdx.x; i < nblk; i += 256) s += (double)n.colsum_part[(long)i * 256 + v];
+  }
   red[threadIdx.x] = s;
   __syncthreads();
   for (int w = 128; w; w >>= 1) {
     if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) n.st->loss_sum = (n.st->mb == 0 ? 0.0 : n.st->loss_sum) + red[0];
-  if (with_grad) {
-    const int v = threadIdx.x;
-    float cs = 0.f;
-    for (int i = 0; i < nblk; ++i) cs += n.colsum_part[(long)i * 256 + v];
-    n.arena[n.po.bdec + v] = to_s<S>(cs);
+  if (threadIdx.x == 0) {
+    if (blockIdx.x == 0) n.st->loss_sum = (n.st->mb == 0 ? 0.0 : n.st->loss_sum) + red[0];
+    else n.arena[n.po.bdec + blockIdx.x - 1] = to_s<S>((float)red[0]);
   }
 }
 
@@ -534,10 +563,7 @@ __global__ void adam_kernel(Net<S> n, float* __restrict__ m, float* __restrict__
     reinterpret_cast<float4*>(v)[q4] = vv;
     reinterpret_cast<float4*>(n.master)[q4] = th;
     // normalised rows get their working copies from wn_norm_kernel once the whole row is updated
-    if (!(n.po.wn && q >= n.po.Wmx && q < n.po.b)) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) store_working(n, q + i, tp[i]);
-    }
+    if (!(n.po.wn && q >= n.po.Wmx && q < n.po.b)) store_working4(n, q, tp);
   }
 }
 

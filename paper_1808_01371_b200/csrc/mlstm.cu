@@ -764,7 +764,7 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
   phase(c, PH_CE);
   const double denom = (double)c->Bfull * c->world * T;  // B_g * T (Q7): all rows of all ranks
   LAUNCH(c, (ce_kernel<S><<<c->nblk_ce, 256, 0, c->stream>>>(n, B, (float)(1.0 / denom), 1)));
-  LAUNCH(c, (ce_reduce_kernel<S><<<1, 256, 0, c->stream>>>(n, c->nblk_ce, 1)));
+  LAUNCH(c, (ce_reduce_kernel<S><<<1 + 256, 256, 0, c->stream>>>(n, c->nblk_ce, 1)));
   phase(c, PH_DHDEC);
   const Opd dYs{n.dY, B, 256, 256, T, (long)B * 256, kPolFirst};  // dY_s = rows of timestep s
   const Opd WdecT{n.WdecT, h, 256, 256, 1, 256L * h, 0, true};
