@@ -169,6 +169,25 @@ __global__ void transpose_kernel(const S* __restrict__ src, S* __restrict__ dst,
   }
 }
 
+// fp16 fast path: 64 x 64 tiles, half2 vectors on both sides (R, C multiples of 64), 32 x 8 threads.
+__global__ void transpose64_kernel(const __half* __restrict__ src, __half* __restrict__ dst, int R, int C) {
+  __shared__ __half tile[64][66];
+  const int c0 = blockIdx.x * 64, r0 = blockIdx.y * 64;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int i = ty; i < 64; i += 8)
+    *reinterpret_cast<__half2*>(&tile[i][2 * tx]) =
+        *reinterpret_cast<const __half2*>(src + (long)(r0 + i) * C + c0 + 2 * tx);
+  __syncthreads();
+#pragma unroll
+  for (int i = ty; i < 64; i += 8) {
+    __half2 o;
+    o.x = tile[2 * tx][i];
+    o.y = tile[2 * tx + 1][i];
+    *reinterpret_cast<__half2*>(dst + (long)(c0 + i) * R + r0 + 2 * tx) = o;
+  }
+}
+
 // ------------------------------------------------------------------ state carry
 template <typename S>
 __global__ void state_in_kernel(Net<S> n, int slot) {

@@ -613,6 +613,12 @@ mlstm_status enqueue_transposes(mlstm_ctx* c) {
   Net<S>& n = net<S>(c);
   const int h = c->h;
   dim3 blk(32, 8);
+  if constexpr (std::is_same<S, __half>::value) {  // h is a multiple of 64
+    LAUNCH(c, (transpose64_kernel<<<dim3(h / 64, h / 64), blk, 0, c->stream>>>(n.Wmh_w, n.WmhT, h, h)));
+    LAUNCH(c, (transpose64_kernel<<<dim3(h / 64, 4 * h / 64), blk, 0, c->stream>>>(n.Wh_w, n.WhT, 4 * h, h)));
+    LAUNCH(c, (transpose64_kernel<<<dim3(h / 64, 256 / 64), blk, 0, c->stream>>>(n.Wdec_w, n.WdecT, 256, h)));
+    return MLSTM_OK;
+  }
   LAUNCH(c, (transpose_kernel<S><<<dim3((h + 31) / 32, (h + 31) / 32), blk, 0, c->stream>>>(n.Wmh_w, n.WmhT, h, h)));
   LAUNCH(c, (transpose_kernel<S><<<dim3((h + 31) / 32, (4 * h + 31) / 32), blk, 0, c->stream>>>(n.Wh_w, n.WhT, 4 * h, h)));
   LAUNCH(c, (transpose_kernel<S><<<dim3((h + 31) / 32, 256 / 32), blk, 0, c->stream>>>(n.Wdec_w, n.WdecT, 256, h)));
