@@ -392,8 +392,10 @@ struct EpiWgrad {
   long off;
   int mode;
   int N;
+  int row0 = 0;  // first output row of this launch (dW_h split into row halves for the allreduce)
   template <int NG>
-  __device__ __forceinline__ void run(int row, int col0, const float* v) const {
+  __device__ __forceinline__ void run(int row_, int col0, const float* v) const {
+    const int row = row_ + row0;
     if (mode == 2) {
       float* dst = n.Scan + (long)row * 5 * n.h;
 #pragma unroll

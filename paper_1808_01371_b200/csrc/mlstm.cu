@@ -107,7 +107,7 @@ struct mlstm_ctx {
   // the weight-gradient GEMM producing them finishes (W_h, then W_mh, then the rest), overlapping
   // the remaining weight-gradient work; MLSTM_AR_OVERLAP=0 reduces after graph A.
   cudaStream_t comm_stream = nullptr;
-  cudaEvent_t ev_wh = nullptr, ev_wmh = nullptr, ev_a_end = nullptr, ev_comm = nullptr;
+  cudaEvent_t ev_wh = nullptr, ev_wmh = nullptr, ev_a_end = nullptr, ev_comm = nullptr, ev_wh_a = nullptr;
   bool ar_overlap = true;
   int force_plan = 0;          // MLSTM_FORCE_PLAN (test instrument), applied while this ctx enqueues
   bool wgrad512 = true;        // weight gradients on 256 x 512 pair tiles (MLSTM_WGRAD512=0: 256 x 256)
@@ -843,7 +843,16 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
         p.bn = 512;
         p.persist = false;
       }
-      if (p.splits == 1 || p.pair || p.cluster) {
+      if (wi == 0 && c->overlap_now() && p.pair && p.splits == 1) {
+        // dW_h in two row halves: the first half's allreduce starts while the second computes
+        // (internal rows [0, 2h) are units [0, h/2) of every gate: 4 contiguous canonical ranges)
+        for (int half = 0; half < 2; ++half) {
+          const Opd Ah = mn(n.G5 + h + (long)half * 2 * h, 2L * h, 5L * h);
+          RET_IF(gemm<S>(c, Ah, 0, w.B, 0, 2 * h, (int)w.N, (int)Kt, p,
+                         EpiWgrad<S>{n, w.off, w.mode, (int)w.N, half * 2 * h}));
+          if (half == 0) CUDA_OR_FAIL(c, cudaEventRecordWithFlags(c->ev_wh_a, c->stream, cudaEventRecordExternal));
+        }
+      } else if (p.splits == 1 || p.pair || p.cluster) {
         RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kt, p, EpiWgrad<S>{n, w.off, w.mode, (int)w.N}));
       } else {
         RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kt, p, EpiPartial{n.part, w.N, w.M * w.N}));
@@ -935,6 +944,17 @@ void accumulate_phases(mlstm_ctx* c, int from, int to) {
     if (cudaEventElapsedTime(&ms, c->ev[p], c->ev[p + 1]) == cudaSuccess) c->phase_ms[p] += ms;
 }
 
+// Whether graph A splits dW_h into row halves (and records ev_wh_a): the same test the wgrad loop
+// applies (overlapped allreduce, CTA-pair plan without split-K).
+template <typename S>
+bool wh_split_ok(mlstm_ctx* c) {
+  if (!c->overlap_now() || !c->tc) return false;
+  g_force_plan = c->force_plan;
+  Plan p = plan_gemm(c->tc, 4L * c->h, c->h, c->Kt, true);
+  g_force_plan = 0;
+  return p.pair && p.splits == 1;
+}
+
 // One step: for each micro-batch, copy its rows of the input (host or device) into the step
 // buffers and run graph A (forward, BPTT, weight gradients, fp32 accumulation across micro-batches);
 // then the allreduce and graph B (overflow check, scaler, Adam, cast) once.
@@ -967,8 +987,21 @@ mlstm_status run_train(mlstm_ctx* c, const uint8_t* bytes, const uint8_t* reset,
       S* a = n.arena;
       cudaStream_t cs = c->comm_stream;
       CUDA_OR_FAIL(c, cudaEventRecord(c->ev_a_end, c->stream));
-      CUDA_OR_FAIL(c, cudaStreamWaitEvent(cs, c->ev_wh, 0));
-      NCCL_OR_FAIL(c, ncclAllReduce(a + po.Wh, a + po.Wh, (size_t)(po.b - po.Wh), dt, ncclSum, c->comm, cs));
+      const long hh = c->h;
+      const bool split_wh = wh_split_ok<S>(c);
+      for (int half = split_wh ? 0 : 1; half < 2; ++half) {  // W_h: units [0, h/2) then [h/2, h) of each gate
+        CUDA_OR_FAIL(c, cudaStreamWaitEvent(cs, half == 0 ? c->ev_wh_a : c->ev_wh, 0));
+        if (!split_wh) {
+          NCCL_OR_FAIL(c, ncclAllReduce(a + po.Wh, a + po.Wh, (size_t)(po.b - po.Wh), dt, ncclSum, c->comm, cs));
+          break;
+        }
+        NCCL_OR_FAIL(c, ncclGroupStart());
+        for (int g = 0; g < 4; ++g) {
+          S* p0 = a + po.Wh + ((long)g * hh + half * (hh / 2)) * hh;
+          NCCL_OR_FAIL(c, ncclAllReduce(p0, p0, (size_t)(hh / 2) * hh, dt, ncclSum, c->comm, cs));
+        }
+        NCCL_OR_FAIL(c, ncclGroupEnd());
+      }
       CUDA_OR_FAIL(c, cudaStreamWaitEvent(cs, c->ev_wmh, 0));
       NCCL_OR_FAIL(c, ncclAllReduce(a + po.Wmh, a + po.Wmh, (size_t)(po.Wx - po.Wmh), dt, ncclSum, c->comm, cs));
       CUDA_OR_FAIL(c, cudaStreamWaitEvent(cs, c->ev_a_end, 0));
@@ -1201,7 +1234,7 @@ mlstm_status mlstm_init(const mlstm_config* cfg, void* workspace, size_t workspa
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     if (cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi) != cudaSuccess)
       return bail(fail(MLSTM_ECUDA, "cudaStreamCreateWithPriority"));
-    for (cudaEvent_t* ev : {&c->ev_wh, &c->ev_wmh, &c->ev_a_end, &c->ev_comm})
+    for (cudaEvent_t* ev : {&c->ev_wh, &c->ev_wmh, &c->ev_a_end, &c->ev_comm, &c->ev_wh_a})
       if (cudaEventCreateWithFlags(ev, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(MLSTM_ECUDA, "cudaEventCreate"));
   }
@@ -1558,7 +1591,7 @@ void mlstm_destroy(mlstm_ctx* c) {
   if (c->st_host) cudaFreeHost(c->st_host);
   if (c->cap) cudaStreamDestroy(c->cap);
   if (c->comm) ncclCommDestroy(c->comm);
-  for (cudaEvent_t ev : {c->ev_wh, c->ev_wmh, c->ev_a_end, c->ev_comm})
+  for (cudaEvent_t ev : {c->ev_wh, c->ev_wmh, c->ev_a_end, c->ev_comm, c->ev_wh_a})
     if (ev) cudaEventDestroy(ev);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   delete c;

@@ -18,14 +18,17 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("world", [2] + ([4] if NGPU >= 4 else []))
-def test_dp_matches_oracle_on_concatenated_rows(tmp_path, world):
+@pytest.mark.parametrize("world,plan", [(2, ""), (2, "pair")] + ([(4, "")] if NGPU >= 4 else []))
+def test_dp_matches_oracle_on_concatenated_rows(tmp_path, world, plan):
+    """plan="pair" forces CTA-pair tiles, so dW_h runs in two row halves whose allreduces start
+    while the rest of the weight gradients compute (the C3/C5 bucket schedule)."""
     h, e, B, T, steps = 128, 64, 130, 8, 3
     out = str(tmp_path / "dp")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr=127.0.0.1", f"--master-port={29600 + world}", os.path.join(HERE, "dp_worker.py"),
-           out, str(h), str(e), str(B), str(T), str(steps)]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+           "--master-addr=127.0.0.1", f"--master-port={29600 + world + (7 if plan else 0)}",
+           os.path.join(HERE, "dp_worker.py"), out, str(h), str(e), str(B), str(T), str(steps)]
+    env = dict(os.environ, MLSTM_FORCE_PLAN=plan) if plan else None
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     R = [np.load(f"{out}.rank{r}.npz") for r in range(world)]
     # replicas: bitwise identical masters and identical global losses on every rank
