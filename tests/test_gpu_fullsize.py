@@ -40,3 +40,14 @@ def test_full_size_sampled_row_losses(name, B, micro):
     assert np.abs(got - want).max() < 2e-2, np.abs(got - want).max()
     rel = np.abs(got.mean(0) - want.mean(0)) / want.mean(0)
     assert rel.max() < 5e-3, rel
+
+
+def test_8192d_sampled_row_losses():
+    """C5's model width (h=8192, 128 rows: the per-timestep GEMM plans bench.py's C5 line takes) on a
+    shorter window (T=32) so the fp64 oracle's 8192^2 matrix-vector products stay affordable."""
+    h, e, B, T = 8192, 64, 128, 32
+    r, got, want = sampled_row_losses(h, e, B, T, 0, [0, 77, 127])
+    assert np.isfinite(r["loss_nats"]) and not r["skipped"]
+    assert np.abs(got - want).max() < 2e-2, np.abs(got - want).max()
+    rel = np.abs(got.mean(0) - want.mean(0)) / want.mean(0)
+    assert rel.max() < 5e-3, rel

@@ -16,7 +16,7 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():
     pytest.skip("needs a B200", allow_module_level=True)
 
-from gpu_helpers import (TOL, oracle_theta, compare_grads, inputs, make_model, oracle_step, rel_l2, split,  # noqa: E402
+from gpu_helpers import (TOL, oracle_theta, compare_grads, cosine, inputs, make_model, oracle_step, rel_l2, split,  # noqa: E402
                          to_dev)
 
 CASES = [
@@ -297,3 +297,18 @@ def test_persistent_backward_matches_oracle(h, B, T, monkeypatch):
     assert abs(res["loss_nats"] - loss_ref) / loss_ref <= TOL["mixed"]["loss_rel"]
     rep = compare_grads(m.get_grads().astype(np.float64), g_ref, h, e, "mixed")
     assert min(rep.values()) >= TOL["mixed"]["grad_cos"], rep
+
+
+def test_multi_step_trace_mixed_tracks_oracle():
+    """10 mixed-precision steps at C2's width (fp16 storage, loss scaling, Adam on fp32 masters)
+    against the fp64 oracle loop: the loss stays within the north_star bound at every step."""
+    h, e, B, T = 1024, 64, 64, 16
+    m = make_model(h, e, B, T, "mixed")
+    st = O.new_train_state(h, e, B, seed=0x5EED)
+    for k in range(10):
+        by = inputs(B, T, k=k)
+        r = m.train_step(to_dev(by))
+        ro = O.train_step(st, by)
+        assert abs(r["loss_nats"] - ro["loss_nats"]) <= TOL["mixed"]["loss_rel"] * ro["loss_nats"], (k, r, ro)
+        assert bool(r["skipped"]) == ro["skipped"] and r["loss_scale"] == ro["alpha"]
+    assert cosine(m.get_params().astype(np.float64) - oracle_theta(h, e), st.theta - oracle_theta(h, e)) > 0.99
