@@ -25,6 +25,8 @@ constexpr int kEpiWarps = 8;
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
 constexpr int kGemmStaticB = 1;  // B operand is a weight untouched by the preceding kernels
 constexpr int kGemmRasterM = 2;  // launch order M-fastest (CTAs running together share a B tile)
+constexpr int kGemmRasterG = 4;  // grouped raster: bands of 8 M-tiles, N-fastest inside a band (L2 reuse
+                                 // of both operands across the CTAs resident together)
 
 // ---- optional intra-kernel timeline (mlstm_trace_enable): one record per CTA,
 // {tag, cta, t_start, t_first_tma, t_first_full, t_acc_ready, t_reduced, t_end} in ns.
@@ -460,8 +462,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const bool leader = rank == 0;
   const int lin = (blockIdx.x >> 1) + (gridDim.x >> 1) * blockIdx.y;  // raster: see gemm_tc_kernel
   const bool rm = flags & kGemmRasterM;
-  const int n0 = (rm ? lin / gridDim.y : (blockIdx.x >> 1)) * BN;
-  const int m0 = (rm ? lin % gridDim.y : blockIdx.y) * 256 + rank * 128;
+  int mi = rm ? lin % gridDim.y : blockIdx.y, ni = rm ? lin / gridDim.y : (blockIdx.x >> 1);
+  if (flags & kGemmRasterG) {  // bands of 8 M-tiles, M-fastest inside a band
+    const int nt = gridDim.x >> 1, band = lin / (8 * nt), in = lin - band * 8 * nt;
+    const int bm = min(8, (int)gridDim.y - band * 8);
+    mi = band * 8 + in % bm;
+    ni = in / bm;
+  }
+  const int n0 = ni * BN;
+  const int m0 = mi * 256 + rank * 128;
   const int total_kb = (K + C::BK - 1) / C::BK;
   const int kb0 = blockIdx.z * kb_per_split;
   const int nkb = max(0, min(kb_per_split, total_kb - kb0));

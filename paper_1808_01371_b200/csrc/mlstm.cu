@@ -111,6 +111,7 @@ struct mlstm_ctx {
   bool ar_overlap = true;
   int force_plan = 0;          // MLSTM_FORCE_PLAN (test instrument), applied while this ctx enqueues
   bool wgrad512 = true;        // weight gradients on 256 x 512 pair tiles (MLSTM_WGRAD512=0: 256 x 256)
+  bool raster_group = true;    // weight-gradient GEMMs in bands of 8 M-tiles (MLSTM_RASTER_GROUP=0: N-fastest)
   bool bwd_persist = false;    // backward recurrence as one persistent kernel (MLSTM_BWD_PERSIST=1; measured slower)
   uint32_t* bwd_sync = nullptr;  // its grid / split-K counters
   int async_epi = 2;  // recurrent epilogue row I/O: 0 per-thread LSU, 1 bulk copies, 2 staged + coalesced (MLSTM_ASYNC_EPI)
@@ -334,6 +335,7 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   if (const char* v = getenv("MLSTM_AR_OVERLAP")) c->ar_overlap = v[0] != '0';
   if (const char* v = getenv("MLSTM_ASYNC_EPI")) c->async_epi = atoi(v);
   if (const char* v = getenv("MLSTM_WGRAD512")) c->wgrad512 = v[0] != '0';
+  if (const char* v = getenv("MLSTM_RASTER_GROUP")) c->raster_group = v[0] != '0';
   if (const char* v = getenv("MLSTM_BWD_PERSIST")) c->bwd_persist = v[0] != '0';
   {
     const char* v = getenv("MLSTM_FORCE_PLAN");
@@ -540,7 +542,7 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
       return MLSTM_ECUDA;
     }
     cudaError_t e;
-    const int gflags = B.weight ? (kGemmStaticB | kGemmRasterM) : 0;
+    const int gflags = B.weight ? (kGemmStaticB | kGemmRasterM) : (A.mn && c->raster_group ? kGemmRasterG : 0);
     const PrefetchJob pj = pf.job;
     const CUtensorMap* ma2 = seg.A2 ? get_map(c, *seg.A2, 128) : ma;
     const CUtensorMap* mb2 = seg.B2 ? get_map(c, *seg.B2, bbox) : mb;
