@@ -312,3 +312,45 @@ def test_multi_step_trace_mixed_tracks_oracle():
         assert abs(r["loss_nats"] - ro["loss_nats"]) <= TOL["mixed"]["loss_rel"] * ro["loss_nats"], (k, r, ro)
         assert bool(r["skipped"]) == ro["skipped"] and r["loss_scale"] == ro["alpha"]
     assert cosine(m.get_params().astype(np.float64) - oracle_theta(h, e), st.theta - oracle_theta(h, e)) > 0.99
+
+
+@pytest.mark.parametrize("precision", ["fp32", "mixed"])
+@pytest.mark.parametrize("h,B,T", [(64, 4, 1), (64, 1, 5), (128, 3, 2)])
+def test_degenerate_shapes_match_oracle(h, B, T, precision):
+    """Degenerate cases of the method: a one-timestep window (no recurrent backward at all), a single
+    row, and a tiny ragged batch."""
+    e = 64
+    m = make_model(h, e, B, T, precision)
+    theta0 = oracle_theta(h, e)
+    by = inputs(B, T)
+    res = m.train_step(to_dev(by))
+    loss_ref, g_ref, (hT, cT), _ = oracle_step(theta0, by, h, e)
+    tol = TOL[precision]
+    assert abs(res["loss_nats"] - loss_ref) / loss_ref <= tol["loss_rel"]
+    rep = compare_grads(m.get_grads().astype(np.float64), g_ref, h, e, precision)
+    for n, v in rep.items():
+        assert (v <= tol["grad_rel_l2"]) if precision == "fp32" else (v >= tol["grad_cos"]), (n, v, rep)
+
+
+def test_eval_partial_batch_and_reset_with_micro_batches():
+    """Eval over Be < micro-batch rows equals the oracle on those rows; reset masks that fall in the
+    second micro-batch zero exactly those rows' state (micro-batched step vs the oracle)."""
+    h, e, B, T = 64, 64, 8, 6
+    m = make_model(h, e, B, T, "fp32", micro_batch=4)
+    by = inputs(B, T)
+    nats, tok, _ = m.eval(to_dev(by[:3]))
+    P = split(oracle_theta(h, e), h, e)
+    ref, tok_ref, _ = O.evaluate(P, by[:3], np.zeros((3, h)), np.zeros((3, h)))
+    assert tok == tok_ref and abs(nats - ref) / ref <= 1e-5
+    rng = np.random.default_rng(5)
+    h0, c0 = rng.standard_normal((B, h)).astype(np.float32), rng.standard_normal((B, h)).astype(np.float32)
+    m.set_state(h0, c0)
+    reset = np.array([0, 0, 0, 0, 1, 0, 1, 0], dtype=np.uint8)
+    r = m.train_step(to_dev(by), to_dev(reset))
+    h0r, c0r = h0.astype(np.float64), c0.astype(np.float64)
+    h0r[reset == 1] = 0
+    c0r[reset == 1] = 0
+    loss_ref, _, (hT, _), _ = oracle_step(oracle_theta(h, e), by, h, e, h0r, c0r)
+    assert abs(r["loss_nats"] - loss_ref) / loss_ref < 1e-5
+    hs, _ = m.get_state(0)
+    assert np.abs(hs - hT).max() < 1e-5
