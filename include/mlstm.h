@@ -181,6 +181,13 @@ const char* mlstm_phase_name(int phase);
 /* Number of kernel launches one train step enqueues (excluding NCCL). */
 int32_t mlstm_launches_per_step(mlstm_ctx* ctx);
 
+/* Which implementation runs the recurrence ("sequential nature"; north_star kernels (b), (c-1)):
+ * 1 = the persistent dataflow kernels (one launch for the T forward timesteps, one for BPTT; mixed
+ * precision, 256 rows per micro-batch, hidden a multiple of 256 up to 4736), 0 = one tcgen05 / SIMT
+ * GEMM launch per timestep and GEMM (every other shape, fp32 mode, or MLSTM_RECUR=0 in the
+ * environment at mlstm_init).  -1 for a null context. */
+int32_t mlstm_recurrence_kind(mlstm_ctx* ctx);
+
 /* Diagnostics: times `iters` launches of the tensor-core GEMM engine on random fp16 operands
  * D[M x N] = A[M x K] B[N x K]^T (fp32 out), engine 1 = one CTA per 128-row tile, 2 = CTA pair
  * (cta_group::2) per 256-row tile, 3 = the library's own plan for the shape (CTA pairs with the

@@ -12,14 +12,17 @@ the paper is silent the reading is the one listed in DESIGN.md "Readings"
 (Q-numbers follow SURVEY.md §8c).
 
 Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
-  * forward      -- torch.nn.LSTM special case (mx == 1), zero-weight closed form,
-                    uniform-logit ln(256) closed form, TBTT state-carry identity.
+  * forward      -- torch.nn.LSTM special case (mx == 1); torch.nn.LSTMCell with the mLSTM's
+                    input-dependent transition W_h diag(W_mx x_t) W_mh (pins mx and its byte
+                    indexing); zero-weight closed form, uniform-logit ln(256) closed form, TBTT
+                    state-carry identity.
   * backward     -- central finite differences on tiny models (all 8 tensors).
   * dE support   -- nonzero embedding-gradient rows == bytes present.
   * adam         -- torch.optim.Adam (fp64), first-step closed form, lr=0 identity.
   * lr schedule  -- values printed in P:302-307 and Tab. lr_scale.
   * scaler       -- SPEC traces S:202-204 and the state-machine properties S:216-218.
-  * overflow     -- IEEE binary16 thresholds (65504 finite, 65520 -> inf).
+  * overflow     -- IEEE binary16 thresholds (65504 finite, 65520 -> inf); the mixed-mode step
+                    decision (fp16 round trip of the scaled gradients) at alpha far below / above them.
   * init         -- SplitMix64 published reference outputs.
   * speedup      -- Tab. gpu_scale (P:215-228) arithmetic.
   * weight norm  -- S:129-130 worked examples, finite differences through (v, g), scale
@@ -361,8 +364,15 @@ def new_train_state(h: int, e: int, B: int, seed: int, scaler: ScalerState | Non
 
 
 def train_step(st: TrainState, bytes_, lr0=3e-3, decay_iters=100_000, n_global_rows=None,
-               reset=None, grads_hook=None, loss_hook=None, beta1=0.9, beta2=0.999, eps=1e-8):
-    """Returns a dict {loss_nats, bpc, skipped, alpha, lr, grads (unscaled, flat)}; mutates st."""
+               reset=None, grads_hook=None, loss_hook=None, beta1=0.9, beta2=0.999, eps=1e-8,
+               precision: str = "fp32"):
+    """Returns a dict {loss_nats, bpc, skipped, alpha, lr, grads (unscaled, flat)}; mutates st.
+
+    precision="mixed": the overflow check runs on the alpha-scaled weight gradients as they exist in
+    the mixed-precision step, i.e. rounded to IEEE binary16 ("FP16 ... weight gradients" sent in
+    the allreduce; "checking for an overflow in the weight gradients"; readings Q8, Q13).  The
+    update itself still uses the fp64 gradients (the oracle is the exact reference).  "fp32": the
+    check runs on the fp64 values (fp32 parity mode has no fp16 buffer to overflow)."""
     bytes_ = np.asarray(bytes_)
     Bn, T1 = bytes_.shape
     Bg = Bn if n_global_rows is None else n_global_rows
@@ -379,7 +389,7 @@ def train_step(st: TrainState, bytes_, lr0=3e-3, decay_iters=100_000, n_global_r
         gflat = grads_hook(gflat)               # e.g. SUM allreduce across ranks (Q7)
     if loss_hook is not None:
         loss_sum = loss_hook(loss_sum)
-    ovf = overflow(gflat)
+    ovf = overflow(to_fp16(gflat) if precision == "mixed" else gflat)
     apply, st.scaler = scaler_step(st.scaler, ovf)
     lr = lr_at(lr0, st.it, decay_iters)
     g_unscaled = gflat / alpha                  # "The division by alpha occurs on the gradients of

@@ -19,21 +19,10 @@
 
 namespace mlstm {
 
-__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void spin_until_geq(const uint32_t* p, uint32_t target) {
-  long long spins = 0;
-  while (ld_acquire_gpu(p) < target) {
-    if (++spins > (1ll << 26)) __trap();  // ~30 s: never hang the GPU on a broken barrier
-  }
-}
-__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+using ptx::ld_acquire_gpu;
+using ptx::st_release_gpu;
+using ptx::spin_until_geq;
+using ptx::fence_proxy_async_global;
 
 constexpr int kBwdSyncWords = 2;  // [0] grid arrivals, [1] grid generation; then one counter per tile
 

@@ -20,6 +20,7 @@
 #include "gemm.cuh"
 #include "kernels.cuh"
 #include "bwd_persist.cuh"
+#include "recur.cuh"
 
 using namespace mlstm;
 
@@ -69,6 +70,7 @@ struct Plan {
 constexpr long kSplitScratchFloats = 160L * 128 * 256;  // >= tiles * S partials of any cluster-split plan
 
 long rup(long x, long m) { return (x + m - 1) / m * m; }
+constexpr int kAsyncRing = 8;  // MLSTM_ASYNC steps in flight before the oldest is delivered
 
 }  // namespace
 
@@ -90,7 +92,15 @@ struct mlstm_ctx {
   uint8_t *bytes = nullptr, *reset = nullptr;
   int32_t* scratch_flag = nullptr;
   DevState* st = nullptr;
-  DevState* st_host = nullptr;  // pinned
+  DevState* st_host = nullptr;  // pinned ring: slots [0, kAsyncRing) for MLSTM_ASYNC steps, slot kAsyncRing for
+                                // synchronous ones (each step copies its DevState into its own slot)
+  struct Pending {
+    mlstm_step_result* out;
+    int slot;
+  };
+  std::vector<Pending> pending;  // MLSTM_ASYNC steps not yet delivered, in step order
+  int ring_next = 0;
+  cudaEvent_t ring_ev[8] = {};
   int nblk_ce = 0;
   long part_elems = 0;
   int seg_splits = 1;
@@ -113,6 +123,11 @@ struct mlstm_ctx {
   bool wgrad512 = true;        // weight gradients on 256 x 512 pair tiles (MLSTM_WGRAD512=0: 256 x 256)
   bool raster_group = true;    // weight-gradient GEMMs in bands of 8 M-tiles (MLSTM_RASTER_GROUP=0: N-fastest)
   bool bwd_persist = false;    // backward recurrence as one persistent kernel (MLSTM_BWD_PERSIST=1; measured slower)
+  // persistent dataflow recurrence (recur.cuh): MLSTM_RECUR=0 forces the per-timestep GEMM path
+  int recur_env = 1;
+  int recur_ok = -1;           // decided once per ctx (shape + co-residency), see recur_on()
+  float* rc_scratch = nullptr;
+  uint32_t* rc_flags = nullptr;
   uint32_t* bwd_sync = nullptr;  // its grid / split-K counters
   int async_epi = 2;  // recurrent epilogue row I/O: 0 per-thread LSU, 1 bulk copies, 2 staged + coalesced (MLSTM_ASYNC_EPI)
   bool overlap_now() const { return world > 1 && ar_overlap && nmb == 1; }
@@ -227,6 +242,13 @@ single:
   return p;
 }
 
+// Shapes the persistent dataflow recurrence (recur.cuh) covers: mixed precision on tcgen05, 256 rows
+// per micro-batch (one CTA pair along M), h a multiple of 256 with h/64 pairs resident at once.
+bool recur_shape_ok(const mlstm_ctx* c) {
+  return c->recur_env != 0 && c->tc && c->mixed && c->B == 256 && c->h % 256 == 0 && c->h / 32 <= 148 &&
+         c->force_plan == 0;
+}
+
 template <typename S>
 void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
   const int h = c->h, e = c->e, B = c->B, T = c->T;
@@ -283,6 +305,10 @@ void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
   n.part = cv.take<float>(part);
   c->split_scratch = c->tc ? cv.take<float>(kSplitScratchFloats) : nullptr;
   c->bwd_sync = cv.take<uint32_t>(kBwdSyncWords + 256);
+  if (recur_shape_ok(c)) {
+    c->rc_scratch = cv.take<float>(rc_scratch_floats(h));
+    c->rc_flags = cv.take<uint32_t>(kRcFlagWords(h / 64));
+  }
   n.Scan = cv.take<float>(256L * 5 * h);
   n.hstate = cv.take<S>(2L * c->Bfull * h);
   n.cstate = cv.take<float>(2L * c->Bfull * h);
@@ -337,6 +363,7 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   if (const char* v = getenv("MLSTM_WGRAD512")) c->wgrad512 = v[0] != '0';
   if (const char* v = getenv("MLSTM_RASTER_GROUP")) c->raster_group = v[0] != '0';
   if (const char* v = getenv("MLSTM_BWD_PERSIST")) c->bwd_persist = v[0] != '0';
+  if (const char* v = getenv("MLSTM_RECUR")) c->recur_env = atoi(v);
   {
     const char* v = getenv("MLSTM_FORCE_PLAN");
     const std::string fp = v ? v : "";
@@ -609,6 +636,105 @@ Net<float>& net<float>(mlstm_ctx* c) {
   return c->nf;
 }
 
+// ------------------------------------------------------------------ persistent recurrence
+cudaLaunchConfig_t recur_cfg(mlstm_ctx* c, cudaLaunchAttribute* at, bool coop) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(c->h / 32, 1, 1);  // h/64 CTA pairs
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = kRcSmem;
+  cfg.stream = c->stream;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = coop ? 2 : 1;
+  return cfg;
+}
+
+// Whether this ctx runs the recurrence on the persistent dataflow kernels (recur.cuh): the shape
+// predicate plus co-residency of all h/64 CTA pairs, decided once.
+bool recur_on(mlstm_ctx* c) {
+  if (c->recur_ok >= 0) return c->recur_ok != 0;
+  c->recur_ok = 0;
+  if (!recur_shape_ok(c) || !c->rc_scratch) return false;
+  for (const void* kern : {(const void*)fwd_recur_kernel, (const void*)bwd_recur_kernel}) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kRcSmem) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    cudaLaunchAttribute at[2];
+    cudaLaunchConfig_t cfg = recur_cfg(c, at, false);
+    cfg.gridDim = dim3(2, 1, 1);
+    int mc = 0;
+    if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc < c->h / 64) {
+      cudaGetLastError();
+      if (getenv("MLSTM_RECUR_DEBUG")) fprintf(stderr, "recur off: max active clusters %d < %d\n", mc, c->h / 64);
+      return false;
+    }
+  }
+  c->recur_ok = 1;
+  return true;
+}
+
+RcPolicy recur_policy(mlstm_ctx* c) {
+  // the per-timestep activation chunks are re-read by every pair within microseconds (normal); the
+  // split GEMM's weight (W_mh, 2h^2 bytes) and the segment operands (XZT / W_dec) are re-read every
+  // timestep (evict_last); W_h (8h^2 bytes, more than L2) streams (evict_first unless MLSTM_L2_WH)
+  return RcPolicy{0u, pol_last(1.f), c->l2_wh > 0 ? pol_last(c->l2_wh) : kPolFirst, pol_last(1.f)};
+}
+
+mlstm_status launch_fwd_recur(mlstm_ctx* c) {
+  Net<__half>& n = c->nh;
+  const int h = c->h, B = c->B, T = c->T;
+  const Opd H{n.Hrm, B, h, h, T + 1, (long)B * h};
+  const Opd M{n.Mrm, B, h, h, T, (long)B * h};
+  const Opd OH{n.OHR, B, 256, 256, T, (long)B * 256};
+  const Opd Wmh{n.Wmh_w, h, h, h, 1, (long)h * h};
+  const Opd Wh{n.Wh_w, 4L * h, h, h, 1, 4L * h * h};
+  const Opd XZ{n.XZT, 4L * h, 256, 256, 1, 4L * h * 256};
+  const CUtensorMap *mH = get_map(c, H, 128), *mM = get_map(c, M, 128), *mO = get_map(c, OH, 128),
+                    *mW1 = get_map(c, Wmh, 128), *mW2 = get_map(c, Wh, 128), *mX = get_map(c, XZ, 128);
+  if (!mH || !mM || !mO || !mW1 || !mW2 || !mX) {
+    c->failed = MLSTM_ECUDA;
+    return MLSTM_ECUDA;
+  }
+  CUDA_OR_FAIL(c, cudaMemsetAsync(c->rc_flags, 0, sizeof(uint32_t) * kRcFlagWords(h / 64), c->stream));
+  cudaLaunchAttribute at[2];
+  cudaLaunchConfig_t cfg = recur_cfg(c, at, true);
+  CUDA_OR_FAIL(c, cudaLaunchKernelEx(&cfg, fwd_recur_kernel, *mH, *mM, *mO, *mW1, *mW2, *mX, n, c->rc_scratch,
+                                     c->rc_flags, recur_policy(c)));
+  count_launch(c);
+  return MLSTM_OK;
+}
+
+mlstm_status launch_bwd_recur(mlstm_ctx* c) {
+  Net<__half>& n = c->nh;
+  const int h = c->h, B = c->B, T = c->T;
+  const Opd dZ{n.G5 + h, B, 4L * h, 5L * h, T, 5L * B * h};
+  const Opd dA{n.dA, B, h, h, T, (long)B * h};
+  const Opd dY{n.dY, B, 256, 256, T, (long)B * 256};
+  // weights MN-major straight from the row-major working copies: element (unit n, k) at k*h + n
+  const Opd Wh{n.Wh_w, h, 4L * h, h, 1, 4L * h * h, 0, true, true};
+  const Opd Wmh{n.Wmh_w, h, h, h, 1, (long)h * h, 0, true, true};
+  const Opd Wdec{n.Wdec_w, h, 256, h, 1, 256L * h, 0, true, true};
+  const CUtensorMap *mZ = get_map(c, dZ, 128), *mA = get_map(c, dA, 128), *mY = get_map(c, dY, 128),
+                    *mW2 = get_map(c, Wh, 64), *mW1 = get_map(c, Wmh, 64), *mD = get_map(c, Wdec, 64);
+  if (!mZ || !mA || !mY || !mW2 || !mW1 || !mD) {
+    c->failed = MLSTM_ECUDA;
+    return MLSTM_ECUDA;
+  }
+  CUDA_OR_FAIL(c, cudaMemsetAsync(c->rc_flags, 0, sizeof(uint32_t) * kRcFlagWords(h / 64), c->stream));
+  cudaLaunchAttribute at[2];
+  cudaLaunchConfig_t cfg = recur_cfg(c, at, true);
+  CUDA_OR_FAIL(c, cudaLaunchKernelEx(&cfg, bwd_recur_kernel, *mZ, *mA, *mY, *mW2, *mW1, *mD, n, c->rc_scratch,
+                                     c->rc_flags, recur_policy(c)));
+  count_launch(c);
+  return MLSTM_OK;
+}
+
 // Recomputes the transposed working copies from the row-major ones.
 template <typename S>
 mlstm_status enqueue_transposes(mlstm_ctx* c) {
@@ -616,6 +742,7 @@ mlstm_status enqueue_transposes(mlstm_ctx* c) {
   const int h = c->h;
   dim3 blk(32, 8);
   if constexpr (std::is_same<S, __half>::value) {  // h is a multiple of 64
+    if (recur_on(c)) return MLSTM_OK;  // the persistent backward reads W_h, W_mh, W_dec MN-major
     LAUNCH(c, (transpose64_kernel<<<dim3(h / 64, h / 64), blk, 0, c->stream>>>(n.Wmh_w, n.WmhT, h, h)));
     LAUNCH(c, (transpose64_kernel<<<dim3(h / 64, 4 * h / 64), blk, 0, c->stream>>>(n.Wh_w, n.WhT, 4 * h, h)));
     LAUNCH(c, (transpose64_kernel<<<dim3(h / 64, 256 / 64), blk, 0, c->stream>>>(n.Wdec_w, n.WdecT, 256, h)));
@@ -671,7 +798,10 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   // F1 (light on HBM) prefetches into L2 the first k-blocks of every W_h tile F2 will stream
   Prefetch pf1;
   if (c->pf_fwd > 0 && c->tc) pf1.add(n.Wh_w, (long)(c->pf_fwd * 8.0 * h * h));
-  for (int t = 0; t < T; ++t) {
+  bool rc = false;
+  if constexpr (std::is_same<S, __half>::value) rc = recur_on(c);
+  if (rc) RET_IF(launch_fwd_recur(c));
+  for (int t = 0; t < (rc ? 0 : T); ++t) {
     if (fold && c->async_epi)
       RET_IF(gemm<S>(c, Hprev, t, Wmh, 0, B, h, h, p1, EpiF1IO<S>{{n, t}}, pf1));
     else
@@ -781,13 +911,17 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
     RET_IF(gemm<S>(c, A, 0, WdecT, 0, T * B, h, 256, plan_gemm(c->tc, (long)T * B, h, 256, false), EpiDHdec<S>{n}));
   }
   phase(c, PH_BWD);
-  if (n.dHdec) {
+  bool rc = false;
+  if constexpr (std::is_same<S, __half>::value) rc = recur_on(c);
+  if (rc) {
+    RET_IF(launch_bwd_recur(c));
+  } else if (n.dHdec) {
     LAUNCH(c, (gate_bwd_last_kernel<S><<<grid_for((long)B * h / 16), 256, 0, c->stream>>>(n)));
   } else {  // gate backward of the last timestep: dH = dY_{T-1} W_dec only (TBTT: no recurrent term)
     RET_IF(gemm<S>(c, dYs, T - 1, WdecT, 0, B, h, 256, plan_gemm(c->tc, B, h, 256, false), EpiB2<S>{n, T - 1}));
   }
   Segment segd;  // B2's second K segment: + dY_{t-1} W_dec
-  if (!n.dHdec) {
+  if (!n.dHdec && !rc) {
     segd.A2 = &dYs;
     segd.B2 = &WdecT;
     segd.K2 = 256;
@@ -800,9 +934,9 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
     const Plan p1 = plan_gemm(c->tc, B, h, 4 * h, false), p2 = plan_gemm(c->tc, B, h, h, false);
     // B2 prefetches into L2 the first k-blocks (of each K split) of the W_h^T tiles B1 streams next
     const size_t es = sizeof(S);
-    const bool persist = std::is_same<S, __half>::value && bwd_persist_ok(c);
+    const bool persist = !rc && std::is_same<S, __half>::value && bwd_persist_ok(c);
     if (persist) RET_IF(launch_bwd_persist(c));
-    for (int t = persist ? -1 : T - 1; t >= 0; --t) {
+    for (int t = (persist || rc) ? -1 : T - 1; t >= 0; --t) {
       // B1(t) prefetches what B2's gate backward of step t-1 reads (written long ago by the
       // forward: gates, c_{t-1} and c_{t-2} (adjacent blocks), dH_dec); B2 prefetches the a-stash
       // block the next B1 reads.
@@ -961,7 +1095,7 @@ bool wh_split_ok(mlstm_ctx* c) {
 // buffers and run graph A (forward, BPTT, weight gradients, fp32 accumulation across micro-batches);
 // then the allreduce and graph B (overflow check, scaler, Adam, cast) once.
 template <typename S>
-mlstm_status run_train(mlstm_ctx* c, const uint8_t* bytes, const uint8_t* reset, cudaMemcpyKind kind) {
+mlstm_status run_train(mlstm_ctx* c, const uint8_t* bytes, const uint8_t* reset, cudaMemcpyKind kind, int slot) {
   if (!c->gA) RET_IF(build_graphs<S>(c));
   Net<S>& n = net<S>(c);
   const size_t rowb = (size_t)(c->T + 1);
@@ -1022,7 +1156,7 @@ mlstm_status run_train(mlstm_ctx* c, const uint8_t* bytes, const uint8_t* reset,
   }
   CUDA_OR_FAIL(c, cudaGraphLaunch(c->gB, c->stream));
   if (c->profile) CUDA_OR_FAIL(c, cudaEventRecord(c->ev[NPH], c->stream));
-  CUDA_OR_FAIL(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(c->st_host + slot, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
   return MLSTM_OK;
 }
 
@@ -1032,8 +1166,7 @@ mlstm_status ctx_ok(mlstm_ctx* c) {
   return MLSTM_OK;
 }
 
-void fill_result(mlstm_ctx* c, mlstm_step_result* out) {
-  const DevState& s = *c->st_host;
+void fill_result(mlstm_ctx* c, const DevState& s, mlstm_step_result* out) {
   c->last = s;
   c->have_last = true;
   if (!out) return;
@@ -1047,18 +1180,41 @@ void fill_result(mlstm_ctx* c, mlstm_step_result* out) {
   out->applied = s.tau;
 }
 
-mlstm_status after_step(mlstm_ctx* c, mlstm_step_result* out) {
-  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
-  fill_result(c, out);
+// Result delivery + divergence detector for one completed step, in step order.  A step
+// counts towards divergence when its loss is non-finite (whether or not the update was skipped --
+// a NaN loss makes the gradients non-finite, so such steps are always skipped) or when it was
+// skipped at the minimum loss scale (alpha cannot back off any further).
+mlstm_status deliver(mlstm_ctx* c, int slot, mlstm_step_result* out) {
+  const DevState s = c->st_host[slot];
+  fill_result(c, s, out);
   if (c->profile) accumulate_phases(c, PH_PREP, NPH);
-  const DevState& s = *c->st_host;
-  if (!s.skipped && !std::isfinite(s.loss_sum)) {
+  const bool bad = !std::isfinite(s.loss_sum) || (s.skipped && s.alpha_used <= c->cfg.scale_min);
+  if (bad) {
     if (++c->nonfinite_run >= c->cfg.diverge_patience)
-      return fail(MLSTM_EDIVERGED, "loss non-finite on diverge_patience consecutive applied steps");
+      return fail(MLSTM_EDIVERGED, "diverged: diverge_patience consecutive steps with a non-finite loss or an "
+                                   "overflow at the minimum loss scale");
   } else {
     c->nonfinite_run = 0;
   }
   return MLSTM_OK;
+}
+
+// Delivers every outstanding MLSTM_ASYNC result (oldest first); the first failure is returned
+// after all of them were delivered.
+mlstm_status drain_pending(mlstm_ctx* c) {
+  mlstm_status first = MLSTM_OK;
+  for (const auto& p : c->pending) {
+    CUDA_OR_FAIL(c, cudaEventSynchronize(c->ring_ev[p.slot]));
+    const mlstm_status s = deliver(c, p.slot, p.out);
+    if (first == MLSTM_OK) first = s;
+  }
+  c->pending.clear();
+  return first;
+}
+
+mlstm_status after_step(mlstm_ctx* c, mlstm_step_result* out) {
+  CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
+  return deliver(c, kAsyncRing, out);
 }
 
 template <typename S>
@@ -1208,7 +1364,11 @@ mlstm_status mlstm_init(const mlstm_config* cfg, void* workspace, size_t workspa
     mlstm_destroy(c);
     return s;
   };
-  if (cudaMallocHost(&c->st_host, sizeof(DevState)) != cudaSuccess) return bail(fail(MLSTM_ECUDA, "cudaMallocHost"));
+  if (cudaMallocHost(&c->st_host, sizeof(DevState) * (kAsyncRing + 1)) != cudaSuccess)
+    return bail(fail(MLSTM_ECUDA, "cudaMallocHost"));
+  for (int i = 0; i < kAsyncRing; ++i)
+    if (cudaEventCreateWithFlags(&c->ring_ev[i], cudaEventDisableTiming) != cudaSuccess)
+      return bail(fail(MLSTM_ECUDA, "cudaEventCreate"));
   if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(MLSTM_ECUDA, "cudaStreamCreate"));
   for (int i = 0; i <= NPH; ++i)
@@ -1248,19 +1408,43 @@ mlstm_status mlstm_train_step(mlstm_ctx* c, const uint8_t* bytes, const uint8_t*
                               mlstm_step_result* out) {
   RET_IF(ctx_ok(c));
   if (!bytes) return fail(MLSTM_EINVAL, "null bytes");
-  RET_IF(c->mixed ? run_train<__half>(c, bytes, reset, cudaMemcpyDeviceToDevice)
-                  : run_train<float>(c, bytes, reset, cudaMemcpyDeviceToDevice));
-  if (flags & MLSTM_ASYNC) return MLSTM_OK;
-  return after_step(c, out);
+  if (flags & MLSTM_ASYNC) {
+    mlstm_status first = MLSTM_OK;
+    if ((int)c->pending.size() == kAsyncRing) {  // ring full: deliver the oldest
+      const auto p = c->pending.front();
+      CUDA_OR_FAIL(c, cudaEventSynchronize(c->ring_ev[p.slot]));
+      c->pending.erase(c->pending.begin());
+      first = deliver(c, p.slot, p.out);
+    }
+    const int slot = c->ring_next;
+    c->ring_next = (c->ring_next + 1) % kAsyncRing;
+    RET_IF(c->mixed ? run_train<__half>(c, bytes, reset, cudaMemcpyDeviceToDevice, slot)
+                    : run_train<float>(c, bytes, reset, cudaMemcpyDeviceToDevice, slot));
+    CUDA_OR_FAIL(c, cudaEventRecord(c->ring_ev[slot], c->stream));
+    c->pending.push_back({out, slot});
+    return first;
+  }
+  const mlstm_status prev = drain_pending(c);
+  RET_IF(c->mixed ? run_train<__half>(c, bytes, reset, cudaMemcpyDeviceToDevice, kAsyncRing)
+                  : run_train<float>(c, bytes, reset, cudaMemcpyDeviceToDevice, kAsyncRing));
+  const mlstm_status s = after_step(c, out);
+  return prev != MLSTM_OK ? prev : s;
+}
+
+mlstm_status mlstm_sync(mlstm_ctx* c) {
+  RET_IF(ctx_ok(c));
+  return drain_pending(c);
 }
 
 mlstm_status mlstm_train_step_host(mlstm_ctx* c, const uint8_t* bytes_host, const uint8_t* reset_host,
                                    mlstm_step_result* out) {
   RET_IF(ctx_ok(c));
   if (!bytes_host) return fail(MLSTM_EINVAL, "null bytes");
-  RET_IF(c->mixed ? run_train<__half>(c, bytes_host, reset_host, cudaMemcpyHostToDevice)
-                  : run_train<float>(c, bytes_host, reset_host, cudaMemcpyHostToDevice));
-  return after_step(c, out);
+  const mlstm_status prev = drain_pending(c);
+  RET_IF(c->mixed ? run_train<__half>(c, bytes_host, reset_host, cudaMemcpyHostToDevice, kAsyncRing)
+                  : run_train<float>(c, bytes_host, reset_host, cudaMemcpyHostToDevice, kAsyncRing));
+  const mlstm_status s = after_step(c, out);
+  return prev != MLSTM_OK ? prev : s;
 }
 
 mlstm_status mlstm_eval(mlstm_ctx* c, const uint8_t* bytes, int32_t Be, const uint8_t* reset, double* nats_sum,
@@ -1489,6 +1673,11 @@ int32_t mlstm_launches_per_step(mlstm_ctx* c) {
   return c->launches;
 }
 
+int32_t mlstm_recurrence_kind(mlstm_ctx* c) {
+  if (!c) return -1;
+  return recur_on(c) ? 1 : 0;
+}
+
 mlstm_status mlstm_gemm_bench(int engine, int M, int N, int K, int bn, int iters, double* ms) {
   if (!ms || M <= 0 || N <= 0 || K <= 0 || iters <= 0 || engine < 1 || engine > 3 ||
       (bn != 0 && bn != 64 && bn != 128 && bn != 256 && !(bn == 512 && engine == 2)) || N % 64 || K % 8)
@@ -1591,6 +1780,8 @@ void mlstm_destroy(mlstm_ctx* c) {
   for (int i = 0; i <= NPH; ++i)
     if (c->ev[i]) cudaEventDestroy(c->ev[i]);
   if (c->st_host) cudaFreeHost(c->st_host);
+  for (cudaEvent_t e : c->ring_ev)
+    if (e) cudaEventDestroy(e);
   if (c->cap) cudaStreamDestroy(c->cap);
   if (c->comm) ncclCommDestroy(c->comm);
   for (cudaEvent_t ev : {c->ev_wh, c->ev_wmh, c->ev_a_end, c->ev_comm, c->ev_wh_a})

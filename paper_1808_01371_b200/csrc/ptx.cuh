@@ -40,6 +40,45 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Non-blocking probe of a phase (the persistent producers poll several conditions in one loop).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+
+// ------------------------------------------------------------------ gpu-scope flags
+// Readiness flags between the CTAs of a persistent kernel: the producer publishes a monotonic value
+// with release semantics after its data stores; the consumer acquires it, then orders the async
+// proxy (TMA loads of that data) after the acquire with fence.proxy.async.
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Bounded spin (~10 s): a broken dependency traps instead of hanging the GPU.
+__device__ __forceinline__ void spin_until_geq(const uint32_t* p, uint32_t target) {
+  if (ld_acquire_gpu(p) >= target) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_gpu(p) < target) {
+    if (globaltimer_ns() - t0 > 10000000000ull) __trap();
+  }
+}
 
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
@@ -177,6 +216,11 @@ __host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N, bool mn = fal
          | ((mn ? 1u : 0u) << 15) | ((mn ? 1u : 0u) << 16)  // A, B major-ness
          | (static_cast<uint32_t>(N >> 3) << 17)    // N / 8
          | (static_cast<uint32_t>(M >> 4) << 24);   // M / 16
+}
+// Same with independent majors (the backward recurrence: K-major activations, MN-major weights).
+__host__ __device__ constexpr uint32_t idesc_f16_f32_ab(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
 }
 
 

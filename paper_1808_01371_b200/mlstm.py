@@ -90,6 +90,7 @@ _SIGS = {
     "mlstm_phase_times": (ctypes.c_int, [_vp, _dp, _i32p, _i32p]),
     "mlstm_phase_name": (ctypes.c_char_p, [ctypes.c_int]),
     "mlstm_launches_per_step": (ctypes.c_int32, [_vp]),
+    "mlstm_recurrence_kind": (ctypes.c_int32, [_vp]),
     "mlstm_gemm_bench": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, _dp]),
     "mlstm_trace_enable": (ctypes.c_int, [ctypes.c_int]),
@@ -349,6 +350,10 @@ class MLSTM:
         n = ctypes.c_int32()
         _check(lib().mlstm_phase_times(self.ctx, ms, ln, ctypes.byref(n)))
         return {lib().mlstm_phase_name(i).decode(): (ms[i], ln[i]) for i in range(n.value)}
+
+    def uses_recur(self) -> bool:
+        """True when the recurrence runs on the persistent dataflow kernels (mlstm_recurrence_kind)."""
+        return lib().mlstm_recurrence_kind(self.ctx) == 1
 
     def launches_per_step(self) -> int:
         n = lib().mlstm_launches_per_step(self.ctx)

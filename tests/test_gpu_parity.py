@@ -166,6 +166,25 @@ def test_loss_scale_overflow_decisions_and_replay():
     assert m2.train_step(to_dev(inputs(B, T)))["skipped"] == 0
 
 
+@pytest.mark.parametrize("alpha", [1.0, 2.0 ** 24, 2.0 ** 40])
+def test_mixed_skip_decision_matches_oracle(alpha):
+    """End-to-end loss-scale decision (SURVEY 8(c) bit-exact #4): the GPU's skip on one mixed
+    step equals the oracle's mixed-mode decision (fp16 round trip of the alpha-scaled gradients) on
+    the same parameters and bytes, at alpha = 1 (scaled gradients < 0.2: applied), 2^24 (max 1.8e6,
+    27x past 65520: skipped) and 2^40 (skipped); both then hold the same halved / unchanged alpha."""
+    h, e, B, T = 64, 64, 4, 16
+    m = make_model(h, e, B, T, "mixed", scale_max=2.0 ** 50)
+    m.set_opt_state(alpha=alpha)
+    by = inputs(B, T)
+    r = m.train_step(to_dev(by))
+    st = O.new_train_state(h, e, B, seed=0x5EED, scaler=O.ScalerState(alpha=alpha, alpha_max=2.0 ** 50))
+    ro = O.train_step(st, by, precision="mixed")
+    assert r["loss_scale"] == alpha == ro["alpha"]
+    assert bool(r["skipped"]) == ro["skipped"] == (alpha > 1.0)
+    assert m.get_opt_state()["alpha"] == st.scaler.alpha
+    assert abs(r["loss_nats"] - ro["loss_nats"]) <= TOL["mixed"]["loss_rel"] * ro["loss_nats"]
+
+
 @pytest.mark.parametrize("precision", ["fp32", "mixed"])
 def test_eval_matches_oracle(precision):
     h, e, B, T = 128, 64, 16, 12

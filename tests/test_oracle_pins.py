@@ -88,6 +88,62 @@ def test_forward_reduces_to_torch_lstm_when_mx_is_one():
     assert abs(loss_sum - ce.item()) < 1e-10 * abs(ce.item())
 
 
+def test_forward_is_an_lstm_with_input_dependent_transition():
+    """The multiplicative LSTM (P:36, P:55 defer to Krause et al. 2016; reading Q1) is an LSTM whose
+    recurrent matrix depends on the current input: W_hh(x_t) = W_h diag(W_mx x_t) W_mh.  Pinned step by
+    step against the library cell torch.nn.LSTMCell (fp64), fed per row and timestep with that
+    transition.  General E and W_mx (no constant column), so dropping the mx factor, transposing W_mx,
+    or gathering mx with another byte or unit changes the transition and fails."""
+    rng = np.random.default_rng(11)
+    h, e, B, T = 5, 4, 3, 6
+    P = _rand_params(h, e, rng)
+    by = rng.integers(0, 256, size=(B, T + 1)).astype(np.uint8)
+    h0 = rng.standard_normal((B, h)) * 0.3
+    c0 = rng.standard_normal((B, h)) * 0.3
+    loss_sum, cache, (hT, cT) = O.forward(P, by, h0, c0)
+    perm = np.concatenate([np.arange(0, h), np.arange(h, 2 * h), np.arange(3 * h, 4 * h),
+                           np.arange(2 * h, 3 * h)])        # ours (i,f,o,u) -> torch (i,f,g,o)
+    cell = torch.nn.LSTMCell(e, h).double()
+    ref_loss = 0.0
+    with torch.no_grad():
+        cell.weight_ih.copy_(torch.from_numpy(P["W_x"][perm]))
+        cell.bias_ih.copy_(torch.from_numpy(P["b"][perm]))
+        cell.bias_hh.zero_()
+        for b in range(B):
+            hb, cb = torch.from_numpy(h0[b:b + 1]), torch.from_numpy(c0[b:b + 1])
+            for t in range(T):
+                x = torch.from_numpy(P["E"][by[b, t]][None])
+                w_hh = P["W_h"] @ np.diag(P["W_mx"] @ P["E"][by[b, t]]) @ P["W_mh"]
+                cell.weight_hh.copy_(torch.from_numpy(w_hh[perm]))
+                hb, cb = cell(x, (hb, cb))
+                assert np.abs(hb.numpy()[0] - cache.hs[t + 1][b]).max() < 1e-12
+                assert np.abs(cb.numpy()[0] - cache.c[t + 1][b]).max() < 1e-12
+                y = hb @ torch.from_numpy(P["W_dec"]).T + torch.from_numpy(P["b_dec"])
+                ref_loss += torch.nn.functional.cross_entropy(y, torch.tensor([int(by[b, t + 1])]),
+                                                              reduction="sum").item()
+    assert abs(loss_sum - ref_loss) < 1e-10 * abs(ref_loss)
+
+
+def test_mixed_step_overflow_decision_uses_fp16_gradients():
+    """the step is skipped when the (alpha-scaled) fp16 weight gradients overflow.  Far from the
+    binary16 threshold the decision is fixed: alpha = 1 keeps every scaled gradient well inside 65504
+    (applied); alpha = 2^40 pushes them past 65520 (skipped, alpha halves, masters and Adam state
+    untouched).  fp32 mode (no fp16 buffer) applies both."""
+    h, e, B, T = 8, 4, 2, 5
+    rng = np.random.default_rng(12)
+    by = rng.integers(0, 256, size=(B, T + 1)).astype(np.uint8)
+    for alpha, skip_mixed in ((1.0, False), (2.0 ** 40, True)):
+        for precision, want in (("mixed", skip_mixed), ("fp32", False)):
+            st = O.new_train_state(h, e, B, seed=3, scaler=O.ScalerState(alpha=alpha, alpha_max=2.0 ** 50))
+            theta0 = st.theta.copy()
+            r = O.train_step(st, by, precision=precision)
+            g_scaled = np.abs(r["grads"]).max() * alpha
+            assert (g_scaled < 65504 / 4) if alpha == 1.0 else (g_scaled > 4 * 65520)
+            assert r["skipped"] == want
+            assert np.array_equal(st.theta, theta0) == want
+            assert st.scaler.alpha == (alpha / 2 if want else alpha)
+
+
 def test_forward_zero_weights_closed_form():
     """All weights and biases zero: i=f=o=1/2, u=0 => c_t = c_{t-1}/2, h_t = tanh(c_t)/2."""
     h, e, B, T = 4, 3, 2, 5
