@@ -50,14 +50,6 @@ def flops_per_char(h, e):
     return 6.0 * (5 * h * h + 5 * h * e + 256 * h)
 
 
-PHASE_KERNELS = {  # what each GEMM phase launches at C3 (profiles/r01_launch_summary_final.txt)
-    "bwd_rec": "gemm_tc1s_kernel<4,EpiB1IO> + gemm_tc1s_kernel<4,EpiB2> per timestep",
-    "fwd_rec": "gemm_tc1s_kernel<4,EpiF1IO> + gemm_tc2_kernel<256,EpiF2IO> per timestep",
-    "wgrad": "gemm_tc2_kernel<512,EpiWgrad,MN> (dW_h, dW_mh, dW_dec) + per-byte sums",
-    "decoder": "gemm_tc2p_kernel<256,EpiY>",
-}
-
-
 def phase_flops(h, e, B, T):
     """Algorithmic FLOPs of each GEMM phase of one step (per rank)."""
     BT = B * T
@@ -68,6 +60,37 @@ def phase_flops(h, e, B, T):
         "wgrad": 2.0 * BT * (5 * h * h + 5 * h * e + 256 * h),             # dW_h, dW_mh, dW_x, dW_mx, dW_dec
         "decoder": 2.0 * BT * 256 * h,
     }
+
+
+def kernel_table(h, e, B, T, persistent):
+    """The kernels of each GEMM phase of one step: name -> (phase, launches per step, algorithmic FLOP per
+    launch).  Names match profiles/ncu_kernel_share.json (tools/kernel_share.py)."""
+    if persistent:
+        pf = phase_flops(h, e, B, T)
+        return {"fwd_recur_kernel": ("fwd_rec", 1, pf["fwd_rec"]), "bwd_recur_kernel": ("bwd_rec", 1, pf["bwd_rec"]),
+                "gemm_tc2_kernel<512,EpiWgrad,MN>": ("wgrad", 3, 2.0 * B * T * (5 * h * h + 256 * h) / 3),
+                "gemm_tc2p_kernel<256,EpiY>": ("decoder", 1, 2.0 * B * T * 256 * h)}
+    return {
+        "gemm_tc1s_kernel<4,EpiF1IO>": ("fwd_rec", T, 2.0 * B * h * h),            # a_t = H_{t-1} W_mh^T
+        "gemm_tc2_kernel<256,EpiF2IO>": ("fwd_rec", T, 2.0 * B * 4 * h * h),       # z_t = M_t W_h^T (+ one-hot seg)
+        "gemm_tc1s_kernel<4,EpiB1IO>": ("bwd_rec", T, 2.0 * B * 4 * h * h),        # dM_t = dZ_t W_h
+        "gemm_tc1s_kernel<4,EpiB2>": ("bwd_rec", T - 1, 2.0 * B * (h + 256) * h),  # dA_t W_mh + dY_{t-1} W_dec
+        "gemm_tc2_kernel<512,EpiWgrad,MN>": ("wgrad", 3, 2.0 * B * T * (5 * h * h + 256 * h) / 3),
+        "gemm_tc2p_kernel<256,EpiY>": ("decoder", 1, 2.0 * B * T * 256 * h),
+    }
+
+
+def kernel_shares(persistent):
+    """phase -> {kernel: share of the phase's kernel time}."""
+    out = {}
+    try:
+        tab = json.load(open(os.path.join(ROOT, "profiles", "ncu_kernel_share.json")))["per_timestep"]["phases"]
+        out = {ph: {k: v["share"] for k, v in ks.items()} for ph, ks in tab.items()}
+    except (OSError, ValueError, KeyError):
+        pass
+    if persistent:  # one kernel per recurrence phase
+        out.update({"fwd_rec": {"fwd_recur_kernel": 1.0}, "bwd_rec": {"bwd_recur_kernel": 1.0}})
+    return out
 
 
 def load_peaks():
@@ -129,15 +152,36 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-class OracleSampler:
-    """The fp64 oracle as it stands, timed on a bounded sample of the same workload (same h, e; 32 rows;
-    window length sized so one sample is ~seconds_hint of CPU work): forward, BPTT and Adam."""
+def host_info():
+    """CPU model and the BLAS numpy links (the oracle's matmul library)."""
+    cpu = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                cpu = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = "unknown"
+    try:
+        cfg = np.__config__.CONFIG["Build Dependencies"]["blas"]
+        blas = f"{cfg.get('name')} {cfg.get('version', '')}".strip()
+    except Exception:
+        pass
+    return cpu, blas
 
-    def __init__(self, h, e, seconds_hint=15.0, B=32):
+
+class OracleSampler:
+    """The fp64 oracle as it stands, timed on a bounded sample of the same workload: same h and e, the
+    oracle batch of SURVEY 8(d) (B = 8 rows), window length sized so one sample is ~seconds_hint of
+    CPU work: forward, BPTT and Adam."""
+
+    def __init__(self, h, e, seconds_hint=15.0, B=8):
         from oracle import mlstm_oracle as O
         from synth import bytestream
         self.O, self.h, self.e, self.B = O, h, e, B
         self.cores = len(os.sched_getaffinity(0))
+        self.cpu, self.blas = host_info()
         self.P = O.init_params(h, e, 0x5EED)
         self.theta = O.flatten(self.P)
         # Per timestep the oracle streams every fp64 weight matrix a few times, so its cost is nearly
@@ -149,6 +193,7 @@ class OracleSampler:
         per_step = (time.perf_counter() - t0) / 4
         self.T = int(max(4, min(256, seconds_hint / max(per_step, 1e-4))))
         self.by = bytestream.window(np.arange(B), 0, self.T)
+        self.seconds = None
 
     def run(self):
         O, B, h = self.O, self.B, self.h
@@ -158,9 +203,11 @@ class OracleSampler:
         st = O.AdamState(np.zeros_like(self.theta), np.zeros_like(self.theta))
         O.adam_apply(self.theta, O.flatten(g), st, 3e-3)
         dt = time.perf_counter() - t0
+        self.seconds = dt
         return {"value": B * self.T / dt, "unit": "chars/s", "cores": self.cores, "kind": "oracle",
+                "cpu": self.cpu, "blas": self.blas, "sample_rows": B, "sample_T": self.T, "seconds": round(dt, 2),
                 "sample": f"fp64 NumPy oracle, h={h} e={self.e}, {B} rows x T={self.T} window (forward, BPTT, "
-                          f"Adam), {dt:.1f} s on {self.cores} host threads"}
+                          f"Adam), {dt:.1f} s on {self.cores} host threads ({self.cpu}; BLAS {self.blas})"}
 
 
 def cpu_baseline(h, e, seconds_hint=15.0):
@@ -179,18 +226,20 @@ def run_reference(args):
     # each "step" is one bounded sample of the workload on the host cores; the whole run stays
     # within a few minutes
     sampler = OracleSampler(h, e, seconds_hint=min(args.ref_seconds, 150.0 / (args.warmup + args.steps)))
-    vals = []
+    vals, secs = [], []
     for i in range(args.warmup + args.steps):
         r = sampler.run()
         if i >= args.warmup:
             vals.append(r["value"])
+            secs.append(r["seconds"])
     v = float(np.median(vals))
-    ms = (B * T) / v * 1e3
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "chars/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "global_batch": B * args.gpus, "seq_len": T, "parallelism": f"dp{args.gpus}"},
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": float(np.median(secs)) * 1e3,  # the wall time of one bounded sample (a "step" here)
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "global_batch": B * args.gpus, "seq_len": T, "parallelism": f"dp{args.gpus}",
+                   "sample": f"each step = {sampler.B} rows x T={sampler.T} of this workload on the host cores"},
         "cpu_baseline": {**r, "value": v},
         "e2e": {"value": v, "unit": "chars/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -205,6 +254,8 @@ def main():
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--weight-norm", action="store_true",
                     help="weight-normalised LSTM matrices (P:150; SURVEY NEXT #1)")
+    ap.add_argument("--recurrence", type=int, default=0, choices=[0, 1, 2],
+                    help="mlstm_config.recurrence: 0 library default, 1 persistent dataflow kernels, 2 per-timestep")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
@@ -227,7 +278,7 @@ def main():
         desc += "; weight-normalised W_mx, W_mh, W_x, W_h (P:150)"
     cfg = M.mlstm_default_config(hidden=h, embed=e, batch=B, seq_len=T, precision=M.MLSTM_MIXED,
                                  micro_batch=MICRO_BATCH.get(args.config, 0),
-                                 weight_norm=1 if args.weight_norm else 0)
+                                 weight_norm=1 if args.weight_norm else 0, recurrence=args.recurrence)
     nid = None
     if world > 1:
         t = torch.zeros(128, dtype=torch.uint8, device="cuda")
@@ -251,25 +302,36 @@ def main():
     for i in range(args.warmup):
         model.train_step(dev[i])
     launches = model.launches_per_step()
+    # per-phase times: a separate profiled run (CUDA events inside the step's graph) before the timed
+    # one, so the timed region has no phase events and no graph re-record
+    n_prof = max(1, min(args.steps, 5))
     model.profile(True)
+    model.train_step(dev[0])  # re-records the graphs with the phase events
+    for i in range(n_prof):
+        model.train_step(dev[i % args.warmup if args.warmup else 0])
     barrier()
+    phases = {k: (v[0] / n_prof, v[1]) for k, v in model.phase_times().items()}
+    model.profile(False)
+    model.train_step(dev[0])  # re-records the graphs without them
+    barrier()
+    # timed region: K steps, profiling off (no phase events, no graph re-record), one event per step
     clocks = ClockSampler(local)
     clocks.start()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
     results = []
-    for i in range(args.warmup, nsteps):
+    for k, i in enumerate(range(args.warmup, nsteps)):
         results.append(model.train_step(dev[i]))
-    ev1.record(stream)
+        evs[k + 1].record(stream)
     barrier()
     clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1)
-    phases = model.phase_times()
-    model.profile(False)
+    ms = evs[0].elapsed_time(evs[-1])
+    step_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
+    med = float(np.median(step_ms))
     if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([ms, med], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+        ms, med = float(tt[0].item()), float(tt[1].item())
     ms_step = ms / args.steps
     value = world * B * T / (ms_step / 1e3)
 
@@ -296,50 +358,65 @@ def main():
 
     if rank != 0:
         return
-    # roofline of the dominant GEMM phase (tensor bound; fp16 peak == bf16 peak, dense)
+    # the profiled steps carry ~20 event records; scale their phase times to the timed step time
+    prof_total = sum(v[0] for v in phases.values())
+    scale = ms_step / prof_total if prof_total > 0 else 1.0
+    phases_raw = {k: round(v[0], 4) for k, v in phases.items()}
+    phases = {k: (v[0] * scale, v[1]) for k, v in phases.items()}
     burst, sustained, hbm, src = load_peaks()
     pf = phase_flops(h, e, B, T)
     gem = {k: phases[k] for k in pf if k in phases}
-    dom = max(gem, key=lambda k: gem[k][0])
-    dom_ms = gem[dom][0] / args.steps
-    dom_launches = gem[dom][1]
-    achieved = pf[dom] / (dom_ms / 1e3) / 1e12
+    # dominant kernel: phase time (live events) x the kernel's share of that phase (committed ncu
+    # launch list, tools/kernel_share.py); per-launch time = that / its launches per step
+    persistent = model.uses_recur()
+    ktab, shares = kernel_table(h, e, B, T, persistent), kernel_shares(persistent)
+    kt = {}
+    for k, (ph, nl, fl) in ktab.items():
+        sh = shares.get(ph, {}).get(k)
+        if ph in gem and sh is not None:
+            kt[k] = (gem[ph][0] * sh, nl, fl, ph, sh)
+    dom = max(kt, key=lambda k: kt[k][0])
+    kms, nl, fl, ph, sh = kt[dom]
+    us_launch = kms / nl * 1e3
+    achieved = fl / (us_launch / 1e6) / 1e12
     traffic = None
-    try:  # measured DRAM bytes per launch of this phase's kernels (committed ncu capture)
-        tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")))
-        traffic = tj.get(args.config, {}).get(dom, {}).get("bytes_per_launch")
+    try:  # measured DRAM bytes per launch of this kernel (committed ncu --set full capture)
+        tj = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tj.get(args.config, {}).get(ph, {}).get("kernels", {}).get(dom)
     except (OSError, ValueError):
         pass
     roof = {"bound": "tensor", "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
             "frac": achieved / sustained, "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
-            "peak_source": f"{src} bf16_tflops_sustained",
-            "kernel": f"{PHASE_KERNELS.get(dom, 'tcgen05 GEMMs')} ({dom} phase: {dom_launches} launches/step, "
-                      f"{pf[dom] / dom_launches / 1e9:.2f} GFLOP per launch avg, "
-                      f"{dom_ms / dom_launches * 1e3:.1f} us per launch avg)"}
-    # every GEMM phase against the same sustained peak (the weight-gradient phase is the one that
-    # reaches the tensor roofline; the recurrence is bound by per-timestep latency + weight streaming)
-    roof_phases = {k: {"tflops": round(pf[k] / (gem[k][0] / args.steps / 1e3) / 1e12, 1),
-                       "frac": round(pf[k] / (gem[k][0] / args.steps / 1e3) / 1e12 / sustained, 3),
-                       "ms": round(gem[k][0] / args.steps, 3)} for k in gem if gem[k][0] > 0}
-    # the recurrences also against HBM: every timestep re-streams the recurrent weights (fp16) and
-    # moves its stash rows (10h^2 weight bytes per timestep and direction-pair; ~48h
-    # stash bytes per row per timestep over both directions)
+            "peak_source": f"{src} bf16_tflops_sustained (fp16 dense = bf16 dense rate)",
+            "kernel": dom, "launches_per_step": nl, "gflop_per_launch": round(fl / 1e9, 3),
+            "us_per_launch": round(us_launch, 2),
+            "how": f"{ph} phase {gem[ph][0]:.3f} ms/step (CUDA events in the step graph) x share {sh:.3f} "
+                   f"(ncu launch list, profiles/ncu_kernel_share.json) / {nl} launches"}
+    # every GEMM phase against the same sustained peak, and the recurrences also against HBM: every
+    # timestep re-streams the recurrent weights (fp16) and moves its stash rows (10h^2
+    # weight bytes per timestep and direction pair; ~48h stash bytes per row per timestep)
+    roof_phases = {k: {"tflops": round(pf[k] / (gem[k][0] / 1e3) / 1e12, 1),
+                       "frac": round(pf[k] / (gem[k][0] / 1e3) / 1e12 / sustained, 3),
+                       "ms": round(gem[k][0], 3)} for k in gem if gem[k][0] > 0}
     for k, wbytes in (("fwd_rec", 2.0 * 5 * h * h), ("bwd_rec", 2.0 * (5 * h * h + 256 * h))):
         if k in roof_phases:
-            byts = T * (wbytes + 24.0 * h * B)
-            gbs = byts / (gem[k][0] / args.steps / 1e3) / 1e9
+            gbs = T * (wbytes + 24.0 * h * B) / (gem[k][0] / 1e3) / 1e9
             roof_phases[k]["hbm_gbs"] = round(gbs, 1)
             roof_phases[k]["hbm_frac"] = round(gbs / hbm, 3)
     whole = flops_per_char(h, e) * world * B * T / (ms_step / 1e3) / 1e12 / world
     line = {
         "metric": METRIC, "value": value, "unit": "chars/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f16 (fp32 accumulate, fp32 masters)", "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_median": med, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f16 (fp32 accumulate, fp32 masters)", "data": "synthetic",
         "config": {"workload": desc, "global_batch": world * B, "seq_len": T, "parallelism": f"dp{world}",
+                   "recurrence": "persistent dataflow kernels" if persistent else "per-timestep GEMM launches",
                    "l2": "no flush: per-step working set (~11 GB) >> 126 MB L2"},
         "roofline": roof, "roofline_phases": roof_phases,
         "step_tflops_per_gpu": whole, "step_frac_of_sustained_peak": whole / sustained,
-        "phases_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in phases.items()},
+        "phases_ms_per_step": {k: round(v[0], 4) for k, v in phases.items()},
+        "phases_profiled_ms": phases_raw,
+        "phases_from": f"profiled run of {n_prof} steps before the timed region (events in the step graph), "
+                       f"scaled by {scale:.3f} to the timed step time",
         "clocks": clk, "e2e": e2e, "gpu_launches": launches * args.steps,
         "loss_first_last": [results[0]["loss_nats"], results[-1]["loss_nats"]],
         "skipped_steps": int(sum(r["skipped"] for r in results)),

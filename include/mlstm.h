@@ -39,7 +39,8 @@ typedef enum {
   MLSTM_ENCCL = 3,     /* NCCL failure; context becomes failed                          */
   MLSTM_ENOMEM = 4,    /* workspace smaller than mlstm_workspace_bytes()                */
   MLSTM_ESTATE = 5,    /* call not valid in the context's current state                 */
-  MLSTM_EDIVERGED = 6  /* diverge_patience consecutive applied steps with non-finite loss */
+  MLSTM_EDIVERGED = 6  /* diverge_patience consecutive steps with a non-finite loss or an
+                          overflow at alpha = scale_min                          */
 } mlstm_status;
 
 enum { MLSTM_FP32 = 0, MLSTM_MIXED = 1 };                   /* precision   */
@@ -69,7 +70,12 @@ typedef struct {
   float scale_init, scale_min, scale_max; /* loss scale alpha: 2^16, 1, 2^24 (Q9)        */
   int32_t scale_growth_interval;          /* clean steps before alpha doubles, 2000 (Q9)        */
   int32_t diverge_patience;               /* MLSTM_EDIVERGED after this many, 50        */
-  int32_t reserved0;
+  int32_t recurrence;  /* 0 = library default (one tcgen05 GEMM launch per timestep and GEMM, the
+                          faster implementation as measured), 1 = the persistent
+                          dataflow kernels (one launch for the T forward timesteps and one for BPTT;
+                          mixed precision, 256 rows per micro-batch, h a multiple of 256 <= 4736,
+                          otherwise the per-timestep path), 2 = per-timestep.  MLSTM_RECUR=0/1 in the
+                          environment at mlstm_init overrides (A/B measurements).             */
 } mlstm_config;
 
 /* Result of one step; every field is the global value over all ranks. */
@@ -117,10 +123,18 @@ mlstm_status mlstm_init(const mlstm_config* cfg, void* workspace, size_t workspa
  * window start), fp16 gradient SUM-allreduce over ranks, overflow check on the reduced buffer,
  * loss-scale update, unscale + Adam on fp32 masters, fp16 cast; the final (h, c) is persisted.
  * out: host; filled after the step completes (the call synchronises the stream) unless
- * MLSTM_ASYNC is set, in which case out is filled at the NEXT synchronising call.
+ * MLSTM_ASYNC is set: then the call only enqueues the step and returns, and *out (which must stay
+ * valid) is filled, in step order, by the next synchronising call (mlstm_sync, a train_step without
+ * the flag, or a 9th outstanding async step, which delivers the oldest).  Up to 8 async results are
+ * kept in a pinned ring; each delivered result runs the divergence detector, so an async run still
+ * returns MLSTM_EDIVERGED (from the delivering call).
  * Input buffers must stay valid until the step has executed on the stream. */
 mlstm_status mlstm_train_step(mlstm_ctx* ctx, const uint8_t* bytes, const uint8_t* reset,
                               uint32_t flags, mlstm_step_result* out);
+
+/* Waits for every outstanding MLSTM_ASYNC step and fills their results (oldest first).  Returns the
+ * first failure among them (e.g. MLSTM_EDIVERGED) after all were delivered; MLSTM_OK if none. */
+mlstm_status mlstm_sync(mlstm_ctx* ctx);
 
 /* Same step, end to end from HOST buffers: host bytes [B][T+1] (and optional host reset [B])
  * are copied to the device inside the call; the result struct is copied back and the stream is
@@ -182,10 +196,8 @@ const char* mlstm_phase_name(int phase);
 int32_t mlstm_launches_per_step(mlstm_ctx* ctx);
 
 /* Which implementation runs the recurrence ("sequential nature"; north_star kernels (b), (c-1)):
- * 1 = the persistent dataflow kernels (one launch for the T forward timesteps, one for BPTT; mixed
- * precision, 256 rows per micro-batch, hidden a multiple of 256 up to 4736), 0 = one tcgen05 / SIMT
- * GEMM launch per timestep and GEMM (every other shape, fp32 mode, or MLSTM_RECUR=0 in the
- * environment at mlstm_init).  -1 for a null context. */
+ * 1 = the persistent dataflow kernels (mlstm_config.recurrence = 1 and a covered shape), 0 = one
+ * tcgen05 / SIMT GEMM launch per timestep and GEMM.  -1 for a null context. */
 int32_t mlstm_recurrence_kind(mlstm_ctx* ctx);
 
 /* Diagnostics: times `iters` launches of the tensor-core GEMM engine on random fp16 operands

@@ -123,9 +123,13 @@ struct mlstm_ctx {
   bool wgrad512 = true;        // weight gradients on 256 x 512 pair tiles (MLSTM_WGRAD512=0: 256 x 256)
   bool raster_group = true;    // weight-gradient GEMMs in bands of 8 M-tiles (MLSTM_RASTER_GROUP=0: N-fastest)
   bool bwd_persist = false;    // backward recurrence as one persistent kernel (MLSTM_BWD_PERSIST=1; measured slower)
-  // persistent dataflow recurrence (recur.cuh): MLSTM_RECUR=0 forces the per-timestep GEMM path
+  // persistent dataflow recurrence (recur.cuh): mlstm_config.recurrence = 1 (or MLSTM_RECUR=1)
   int recur_env = 1;
-  int recur_ok = -1;           // decided once per ctx (shape + co-residency), see recur_on()
+  int recur_ok = -1;
+  int rc_exp = 0;                 // MLSTM_RC_EXP: timing experiments (wrong results), see RcPolicy
+  int rc_rotate = 1;              // MLSTM_RC_ROTATE
+  int rc_pf_dist = 0;             // MLSTM_RC_PF: weight k-blocks prefetched into L2 ahead of the ring
+  int rc_flag_lanes = 32;  // MLSTM_RC_FLAG_LANES: activation flags acquired in parallel (1 = serial)           // decided once per ctx (shape + co-residency), see recur_on()
   float* rc_scratch = nullptr;
   uint32_t* rc_flags = nullptr;
   uint32_t* bwd_sync = nullptr;  // its grid / split-K counters
@@ -332,6 +336,7 @@ mlstm_status validate(const mlstm_config* cfg) {
     return fail(MLSTM_EINVAL, "micro_batch must be 0 (= batch) or divide batch");
   if (cfg->weight_norm != 0 && cfg->weight_norm != 1) return fail(MLSTM_EINVAL, "weight_norm must be 0 or 1 (Q24)");
   if (cfg->precision != MLSTM_FP32 && cfg->precision != MLSTM_MIXED) return fail(MLSTM_EINVAL, "bad precision");
+  if (cfg->recurrence < 0 || cfg->recurrence > 2) return fail(MLSTM_EINVAL, "recurrence must be 0, 1 or 2");
   if (!(cfg->decay_iters > 0) || !(cfg->lr0 >= 0)) return fail(MLSTM_EINVAL, "bad LR schedule");
   if (!(cfg->scale_min > 0) || !(cfg->scale_max >= cfg->scale_min) || !(cfg->scale_init >= cfg->scale_min) ||
       !(cfg->scale_init <= cfg->scale_max) || cfg->scale_growth_interval <= 0)
@@ -341,6 +346,7 @@ mlstm_status validate(const mlstm_config* cfg) {
 
 void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   c->cfg = *cfg;
+  c->recur_env = cfg->recurrence == 1 ? 1 : 0;  // 0 (default) and 2: per-timestep launches
   c->h = cfg->hidden;
   c->e = cfg->embed;
   c->Bfull = cfg->batch;
@@ -364,6 +370,10 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   if (const char* v = getenv("MLSTM_RASTER_GROUP")) c->raster_group = v[0] != '0';
   if (const char* v = getenv("MLSTM_BWD_PERSIST")) c->bwd_persist = v[0] != '0';
   if (const char* v = getenv("MLSTM_RECUR")) c->recur_env = atoi(v);
+  if (const char* v = getenv("MLSTM_RC_EXP")) c->rc_exp = atoi(v);
+  if (const char* v = getenv("MLSTM_RC_ROTATE")) c->rc_rotate = atoi(v) != 0;
+  if (const char* v = getenv("MLSTM_RC_PF")) c->rc_pf_dist = std::max(0, atoi(v));
+  if (const char* v = getenv("MLSTM_RC_FLAG_LANES")) c->rc_flag_lanes = std::max(1, std::min(32, atoi(v)));
   {
     const char* v = getenv("MLSTM_FORCE_PLAN");
     const std::string fp = v ? v : "";
@@ -640,7 +650,7 @@ Net<float>& net<float>(mlstm_ctx* c) {
 cudaLaunchConfig_t recur_cfg(mlstm_ctx* c, cudaLaunchAttribute* at, bool coop) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c->h / 32, 1, 1);  // h/64 CTA pairs
-  cfg.blockDim = dim3(kGemmThreads);
+  cfg.blockDim = dim3(kRcThreads);
   cfg.dynamicSmemBytes = kRcSmem;
   cfg.stream = c->stream;
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -683,7 +693,7 @@ RcPolicy recur_policy(mlstm_ctx* c) {
   // the per-timestep activation chunks are re-read by every pair within microseconds (normal); the
   // split GEMM's weight (W_mh, 2h^2 bytes) and the segment operands (XZT / W_dec) are re-read every
   // timestep (evict_last); W_h (8h^2 bytes, more than L2) streams (evict_first unless MLSTM_L2_WH)
-  return RcPolicy{0u, pol_last(1.f), c->l2_wh > 0 ? pol_last(c->l2_wh) : kPolFirst, pol_last(1.f)};
+  return RcPolicy{0u, pol_last(1.f), c->l2_wh > 0 ? pol_last(c->l2_wh) : kPolFirst, pol_last(1.f), c->rc_flag_lanes, c->rc_pf_dist, c->rc_rotate, c->rc_exp};
 }
 
 mlstm_status launch_fwd_recur(mlstm_ctx* c) {

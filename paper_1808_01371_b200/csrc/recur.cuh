@@ -28,7 +28,8 @@
 // F2, dY W_dec in B2) runs while the other accumulator's epilogue is still reducing.
 //
 // Launched with cluster dims (2,1,1) and the cooperative attribute (all pairs co-resident).
-// Roles (320 threads): warp 0 lane 0 = TMA producer (both CTAs), warp 1 lane 0 of the leader CTA =
+// Roles (352 threads): warp 0 lane 0 = weight TMA producer, warp 10 = activation TMA producer (both
+// CTAs; the activation warp polls readiness flags with all lanes), warp 1 lane 0 of the leader CTA =
 // tcgen05.mma issuer, warps 2..9 = epilogue (two warps per TMEM lane quarter: q = warp & 3 owns
 // rows [32q, +32), grp = (warp - 2) >> 2 takes half of each 64-column slice).
 #pragma once
@@ -38,13 +39,81 @@
 namespace mlstm {
 
 constexpr int kRcStages = 5;
+constexpr int kRcActWarp = 10;                // activation producer (after the 8 epilogue warps)
+constexpr int kRcThreads = kGemmThreads + 32;
 constexpr int kRcTile = 128 * 64 * 2;  // one 128-row x 64-K fp16 operand tile (per CTA, per stage)
 constexpr int kRcWin = 8192;           // staging window of one epilogue warp
 constexpr int kRcSmem = kRcStages * 2 * kRcTile + kEpiWarps * kRcWin + 1024 + 256;
 
 struct RcPolicy {  // L2 policy codes (ptx::make_policy) of the operand streams
   uint32_t act, w_split, w_wide, w_seg;
+  int flag_lanes;  // activation flags the producer warp acquires in parallel (1 = one at a time)
+  int pf_dist;     // weight k-blocks prefetched into L2 ahead of the ring (0 = off)
+  int rotate;      // 1: each pair starts its K loop at its own chunk (spreads the L2 reads); 0: all pairs
+                   // read the shared activation chunks in the same order (same lines requested together)
+  int exp;         // timing experiments only (wrong results): bit 0 = F2 A from chunk 0, bit 1 = F2 B block 0,
+                   // bit 2 = no F2 A loads, bit 3 = no F2 B loads, bit 4 = no readiness flags (races),
+                   // bit 5 = bare forward epilogue (no reduce / stores)
 };
+
+// One operand k-block of the producer's stream: its readiness flag (null = no dependency, e.g. a
+// weight-only or input-only segment) and the value that flag must reach.
+struct RcBlk {
+  int t, kind, j;
+  const uint32_t* flag;
+  uint32_t target;
+};
+
+// Optional timeline (mlstm_trace_enable; tools/trace_recur.py): each CTA reserves T + per TraceRec
+// records -- one per timestep {tag = 1000 + t (fwd) / 2000 + u (bwd), cta, 10 event times in ns} and
+// one per k-block of the sampled timestep {tag = 3000 / 4000 + i, cta, weight issued, activation
+// issued, stage full (MMA thread)}.
+constexpr int kRcTraceStep = 8;
+constexpr int kRcTraceBlk = 160;  // >= k-blocks per timestep (h <= 4736)
+struct RcTrace {
+  uint32_t base;
+  int T, idx0, per, tag;
+  __device__ __forceinline__ bool on() const { return base != 0xffffffffu; }
+  __device__ __forceinline__ void step(int t, int slot) const {
+    if (on()) g_trace[base + t].v[slot] = ptx::globaltimer();
+  }
+  __device__ __forceinline__ void step_tag(int t, int tg) const {
+    if (on()) {
+      g_trace[base + t].v[0] = (uint64_t)tg;
+      g_trace[base + t].v[1] = blockIdx.x;
+    }
+  }
+  // detail record of timestep t (tag + 2000 + t): sub-phases of the epilogues
+  __device__ __forceinline__ void det(int t, int slot) const {
+    if (on() && t >= 0) {
+      TraceRec& rr = g_trace[base + T + t];
+      rr.v[slot] = ptx::globaltimer();
+      rr.v[0] = (uint64_t)(tag + 2000 + t);
+      rr.v[1] = blockIdx.x;
+    }
+  }
+  __device__ __forceinline__ void blk_val(int idx, int slot, uint64_t v) const {
+    const int i = idx - idx0;
+    if (on() && i >= 0 && i < per) g_trace[base + 2 * T + i].v[slot] = v;
+  }
+  __device__ __forceinline__ uint64_t now() const { return on() ? ptx::globaltimer() : 0; }
+  __device__ __forceinline__ void blk(int idx, int slot) const {
+    const int i = idx - idx0;
+    if (on() && i >= 0 && i < per) {
+      TraceRec& rr = g_trace[base + 2 * T + i];
+      rr.v[slot] = ptx::globaltimer();
+      if (slot == 2) {
+        rr.v[0] = (uint64_t)(tag + i);
+        rr.v[1] = blockIdx.x;
+      }
+    }
+  }
+};
+__device__ __forceinline__ uint32_t rc_trace_reserve(int n) {
+  if (!g_trace) return 0xffffffffu;
+  const uint32_t base = atomicAdd(&g_trace_n, (uint32_t)n);
+  return base + (uint32_t)n <= g_trace_cap ? base : 0xffffffffu;
+}
 
 struct RcLayout {
   uint8_t *sA, *sB, *win;
@@ -100,11 +169,12 @@ __device__ __forceinline__ void rc_setup(const RcLayout& L) {
 
 // One k-block on the MMA thread: 4 x (M=256, N=256, K=16) into accumulator `d`.
 template <bool BMN>
-__device__ __forceinline__ void rc_consume(const RcLayout& L, uint32_t it, uint32_t d, bool acc) {
+__device__ __forceinline__ void rc_consume(const RcLayout& L, uint32_t it, uint32_t d, bool acc, const RcTrace& tr) {
   constexpr uint32_t idesc = ptx::idesc_f16_f32_ab(256, 256, false, BMN);
   const int s = it % kRcStages;
   ptx::mbar_wait(&L.full[s], (it / kRcStages) & 1);
   ptx::tc_fence_after();
+  tr.blk((int)it, 4);
   const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(L.sA + s * kRcTile));
   const uint32_t sb = ptx::smem_u32(L.sB + s * kRcTile);
   const uint64_t bd = BMN ? ptx::sdesc_mnmajor_sw128(sb) : ptx::sdesc_kmajor_sw128(sb);
@@ -130,8 +200,8 @@ __device__ __forceinline__ void rc_bar() { asm volatile("bar.sync 1, 256;" ::: "
 __device__ __forceinline__ void rc_publish(uint32_t* flag, uint32_t val, int tid) {
   rc_bar();
   if (tid == 0) {
-    __threadfence();
-    ptx::st_release_gpu(flag, val);
+    ptx::fence_acq_rel_gpu();
+    ptx::st_relaxed_gpu(flag, val);
   }
 }
 
@@ -142,7 +212,7 @@ __device__ __forceinline__ void rc_publish(uint32_t* flag, uint32_t val, int tid
 // own slice summed over z = 0..3 in order (its own partial straight from TMEM).
 __device__ __forceinline__ void rc_reduce(uint32_t tmem, int col0, float4* grp_scratch, int z, int q, int grp,
                                           int lane, int tid, uint32_t* pflags, uint32_t val, uint64_t* acce,
-                                          bool leader, float* out) {
+                                          bool leader, float* out, const RcTrace& tr, int trt, int slot0) {
   const int rl = q * 32 + lane;
   const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16) + col0;
 #pragma unroll 1
@@ -156,6 +226,7 @@ __device__ __forceinline__ void rc_reduce(uint32_t tmem, int col0, float4* grp_s
 #pragma unroll
     for (int i = 0; i < 8; ++i) dst[i * 128] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
   }
+  if (tid == 0) tr.det(trt, slot0);
   float own[32];
   ptx::tmem_ld16(trow + 64 * z + 32 * grp, own);
   ptx::tmem_ld16(trow + 64 * z + 32 * grp + 16, own + 16);
@@ -163,11 +234,13 @@ __device__ __forceinline__ void rc_reduce(uint32_t tmem, int col0, float4* grp_s
   rc_release_acc(acce, leader, lane);
   rc_bar();
   if (tid == 0) {
-    __threadfence();
-    ptx::st_release_gpu(pflags + z, val);
+    tr.det(trt, slot0 + 1);
+    ptx::fence_acq_rel_gpu();
+    ptx::st_relaxed_gpu(pflags + z, val);
 #pragma unroll 1
     for (int zz = 0; zz < 4; ++zz)
       if (zz != z) ptx::spin_until_geq(pflags + zz, val);
+    tr.det(trt, slot0 + 2);
   }
   rc_bar();
 #pragma unroll
@@ -189,6 +262,7 @@ __device__ __forceinline__ void rc_reduce(uint32_t tmem, int col0, float4* grp_s
       out[4 * i + 3] += p.w;
     }
   }
+  if (tid == 0) tr.det(trt, slot0 + 3);
 }
 
 // Stage 16*NG values of this lane's row (converted to fp16) at w + lane*pitch.
@@ -210,6 +284,130 @@ __device__ __forceinline__ void rc_watchdog(bool progress, uint64_t& idle_since)
   else if (now - idle_since > 10000000000ull) __trap();
 }
 
+// Two producers per CTA, so that neither stream waits behind the other's issue overhead.  The
+// k-block stream is `pre` prologue blocks followed by `per` blocks per step; `dec(u, i)` maps step u
+// (-1 = prologue) and block i to its operands.  Both producers walk it with incremental cursors (no
+// divisions on the issue path).
+struct RcCursor {
+  int u, i, per;
+  __device__ __forceinline__ RcCursor(int idx, int pre, int per_) : per(per_) {
+    if (idx < pre) {
+      u = -1;
+      i = idx;
+    } else {
+      u = (idx - pre) / per;
+      i = (idx - pre) - u * per;
+    }
+  }
+  __device__ __forceinline__ void next(int pre) {
+    if (u < 0) {
+      if (++i == pre) {
+        u = 0;
+        i = 0;
+      }
+    } else if (++i == per) {
+      i = 0;
+      ++u;
+    }
+  }
+};
+
+// Weights (warp 0, lane 0): the weight k-blocks do not depend on the recurrence; each is loaded as
+// soon as its ring stage is free (HW-sleeping mbarrier wait), optionally with block wi + pf_dist
+// prefetched into L2 at the same time.  (Measured alternative: one thread issuing both operands of
+// each stage ran at 0.88 us per F2 k-block against 0.55 us for the two producers here.)
+template <class Dec, class IssueW, class PrefW>
+__device__ __forceinline__ void rc_weights(const RcLayout& L, int total, int pre, int per, bool leader, int pf_dist,
+                                           const RcTrace& tr, Dec dec, IssueW issue_w, PrefW prefetch_w,
+                                           bool skip_kind2 = false) {
+  if (pf_dist > 0) {
+    RcCursor pc(0, pre, per);
+#pragma unroll 1
+    for (int i = 0; i < min(pf_dist, total); ++i, pc.next(pre)) prefetch_w(dec(pc.u, pc.i));
+  }
+  RcCursor c(0, pre, per), pc(pf_dist, pre, per);
+  int s = 0;
+  uint32_t ph = 1;
+#pragma unroll 1
+  for (int wi = 0; wi < total; ++wi, c.next(pre)) {
+    if (wi >= kRcStages) ptx::mbar_wait(&L.empty[s], ph);
+    const RcBlk b = dec(c.u, c.i);
+    const bool skip = skip_kind2 && b.kind == 2;  // timing experiment (RcPolicy::exp bit 3)
+    if (leader) {
+      if (skip) ptx::mbar_arrive(&L.full[s]);
+      else ptx::mbar_arrive_expect_tx(&L.full[s], 2 * kRcTile);
+    }
+    if (!skip) issue_w(s, b);
+    if (tr.on()) tr.blk(wi, 2);
+    if (pf_dist > 0 && wi + pf_dist < total) {
+      prefetch_w(dec(pc.u, pc.i));
+      pc.next(pre);
+    }
+    if (++s == kRcStages) {
+      s = 0;
+      ph ^= 1;
+    }
+  }
+}
+
+// Activations (warp kRcActWarp, all lanes; lane 0 issues): an activation k-block is loaded into its
+// stage once the flag of the CTA that produces it says it is published.  Readiness is learned in
+// windows, ahead of need: the lanes acquire the flags of the next `flag_lanes` blocks in parallel
+// and extend the known-published prefix, lane 0 orders the async proxy after the acquires with one
+// fence.proxy.async and then issues every known block on its own (no warp synchronisation per
+// block) -- a few L2 round trips per timestep instead of one acquire + one warp barrier per block.
+template <class Dec, class IssueA>
+__device__ __forceinline__ void rc_acts(const RcLayout& L, int total, int pre, int per, int lane, bool leader,
+                                        int flag_lanes, const RcTrace& tr, Dec dec, IssueA issue_a,
+                                        bool skip_kind2 = false, bool no_flags = false) {
+  int ai = 0, known = no_flags ? total : 0;  // blocks [0, known) are published and fenced; [0, ai) issued
+  uint64_t idle_since = 0;
+  RcCursor c(0, pre, per);
+  int s = 0;
+  uint32_t ph = 1;
+#pragma unroll 1
+  while (ai < total) {
+    if (known < min(total, ai + kRcStages)) {  // learn readiness of the blocks after `known`
+      const int n = min(total - known, flag_lanes);
+      bool ready = true;
+      if (lane < n) {
+        const RcCursor q(known + lane, pre, per);
+        const RcBlk b = dec(q.u, q.i);
+        if (b.flag) ready = ptx::ld_acquire_gpu(b.flag) >= b.target;
+      }
+      const unsigned waiting = __ballot_sync(0xffffffffu, !ready);
+      const int k = min(waiting ? __ffs(waiting) - 1 : 32, n);
+      if (k > 0) {
+        __syncwarp();
+        if (lane == 0) ptx::fence_proxy_async_global();
+        known += k;
+      }
+      if (lane == 0) rc_watchdog(k > 0 || known > ai, idle_since);
+      if (known == ai) continue;
+    }
+    if (lane == 0) {
+#pragma unroll 1
+      for (int a = ai; a < known; ++a, c.next(pre)) {
+        if (a >= kRcStages) ptx::mbar_wait(&L.empty[s], ph);
+        const RcBlk b = dec(c.u, c.i);
+        const bool skip = skip_kind2 && b.kind == 2;  // timing experiment (RcPolicy::exp bit 2)
+        if (leader) {
+          if (skip) ptx::mbar_arrive(&L.full[s]);
+          else ptx::mbar_arrive_expect_tx(&L.full[s], 2 * kRcTile);
+        }
+        if (!skip) issue_a(s, b);
+        if (tr.on()) tr.blk(a, 3);
+        if (++s == kRcStages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    ai = known;
+    __syncwarp();
+  }
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -218,7 +416,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 // Forward: for t = 0..T-1   F1(t): a_t = H_{t-1} W_mh^T (split z of tile n1), m_t = mx_t * a_t
 //                            F2(t): z_t = onehot(x_t) (W_x E + b)^T + M_t W_h^T; gates, c, h
 // =============================================================================================
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kRcThreads, 1)
     fwd_recur_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmM,
                      const __grid_constant__ CUtensorMap tmOH, const __grid_constant__ CUtensorMap tmWmh,
                      const __grid_constant__ CUtensorMap tmWh, const __grid_constant__ CUtensorMap tmXZ, Net<__half> n,
@@ -235,6 +433,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint32_t* fH = flags;           // [P][2]
   uint32_t* fM = flags + 2 * P;   // [P][2]
   uint32_t* fP = flags + 4 * P;   // [(n1, r)][4]
+  __shared__ uint32_t tr_base_s;
+  if (threadIdx.x == 0) tr_base_s = rc_trace_reserve(2 * T + kRcTraceBlk);
   rc_setup(L);
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmH);
@@ -248,68 +448,64 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem = *L.tmem_slot;
+  const RcTrace tr{tr_base_s, T, kRcTraceStep * per, per, 3000};
 
-  if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------------------------ TMA producer
+  if (warp == 0 || warp == kRcActWarp) {
+    {  // ----------------------------------------------------------- TMA producers (weights, activations)
       const uint64_t pact = ptx::make_policy(pol.act), pw1 = ptx::make_policy(pol.w_split),
                      pw2 = ptx::make_policy(pol.w_wide), pws = ptx::make_policy(pol.w_seg);
       const uint32_t bar0 = ptx::mapa_shared(ptx::smem_u32(&L.full[0]), 0);
-      const int total = T * per;
-      // k-block idx -> (t, kind, chunk)
-      auto decode = [&](int idx, int& t, int& kind, int& j) {
-        t = idx / per;
-        const int i = idx - t * per;
+      // k-block idx -> (t, kind, chunk): per timestep nF1 H chunks of F1 (K range z), the 4 one-hot
+      // segment blocks of F2, then nF2 M chunks of F2 (each stream starts at its own chunk)
+      auto dec = [&](int u, int i) {
+        RcBlk b;
+        b.t = u;
+        b.flag = nullptr;
         if (i < nF1) {
-          kind = 0;
-          j = z * nF1 + (i + n1) % nF1;
-        } else if (i < nF1 + 4) {
-          kind = 1;
-          j = i - nF1;
-        } else {
-          kind = 2;
-          j = (i - nF1 - 4 + p) % nF2;
-        }
-      };
-      int wi = 0, ai = 0;
-      uint64_t idle_since = 0;
-#pragma unroll 1
-      while (ai < total) {
-        bool progress = false;
-        // weights: as far ahead as free stages allow (they do not depend on the recurrence)
-#pragma unroll 1
-        while (wi < total && wi < ai + kRcStages) {
-          const int s = wi % kRcStages;
-          if (wi >= kRcStages && !ptx::mbar_test(&L.empty[s], ((wi / kRcStages) & 1) ^ 1)) break;
-          int t, kind, j;
-          decode(wi, t, kind, j);
-          if (leader) ptx::mbar_arrive_expect_tx(&L.full[s], 2 * kRcTile);
-          uint8_t* dst = L.sB + s * kRcTile;
-          if (kind == 0) ptx::tma_load_3d_2sm(dst, &tmWmh, bar0 + 8 * s, 64 * j, 256 * n1 + 128 * r, 0, pw1);
-          else if (kind == 1) ptx::tma_load_3d_2sm(dst, &tmXZ, bar0 + 8 * s, 64 * j, 256 * p + 128 * r, 0, pws);
-          else ptx::tma_load_3d_2sm(dst, &tmWh, bar0 + 8 * s, 64 * j, 256 * p + 128 * r, 0, pw2);
-          ++wi;
-          progress = true;
-        }
-        // activations: once their producer published them
-        if (ai < wi) {
-          int t, kind, j;
-          decode(ai, t, kind, j);
-          bool ready = true;
-          if (kind == 0 && t > 0) ready = ptx::ld_acquire_gpu(&fH[2 * j + r]) >= (uint32_t)t;
-          else if (kind == 2) ready = ptx::ld_acquire_gpu(&fM[2 * j + r]) >= (uint32_t)(t + 1);
-          if (ready) {
-            if (kind != 1) ptx::fence_proxy_async_global();
-            const int s = ai % kRcStages;
-            if (leader) ptx::mbar_arrive_expect_tx(&L.full[s], 2 * kRcTile);
-            uint8_t* dst = L.sA + s * kRcTile;
-            if (kind == 0) ptx::tma_load_3d_2sm(dst, &tmH, bar0 + 8 * s, 64 * j, 128 * r, t, pact);
-            else if (kind == 1) ptx::tma_load_3d_2sm(dst, &tmOH, bar0 + 8 * s, 64 * j, 128 * r, t, pact);
-            else ptx::tma_load_3d_2sm(dst, &tmM, bar0 + 8 * s, 64 * j, 128 * r, t, pact);
-            ++ai;
-            progress = true;
+          b.kind = 0;
+          int jj = i + n1 * pol.rotate;
+          if (jj >= nF1) jj -= nF1;
+          b.j = z * nF1 + jj;
+          if (b.t > 0) {
+            b.flag = &fH[2 * b.j + r];
+            b.target = (uint32_t)b.t;
           }
+        } else if (i < nF1 + 4) {
+          b.kind = 1;
+          b.j = i - nF1;
+        } else {
+          b.kind = 2;
+          int jj = i - nF1 - 4 + p * pol.rotate;
+          if (jj >= nF2) jj -= nF2;
+          b.j = jj;
+          b.flag = &fM[2 * b.j + r];
+          b.target = (uint32_t)(b.t + 1);
         }
-        rc_watchdog(progress, idle_since);
+        return b;
+      };
+      auto issue_w = [&](int s, const RcBlk& b) {
+        uint8_t* dst = L.sB + s * kRcTile;
+        if (b.kind == 0) ptx::tma_load_3d_2sm(dst, &tmWmh, bar0 + 8 * s, 64 * b.j, 256 * n1 + 128 * r, 0, pw1);
+        else if (b.kind == 1) ptx::tma_load_3d_2sm(dst, &tmXZ, bar0 + 8 * s, 64 * b.j, 256 * p + 128 * r, 0, pws);
+        else ptx::tma_load_3d_2sm(dst, &tmWh, bar0 + 8 * s, (pol.exp & 2) ? 0 : 64 * b.j, 256 * p + 128 * r, 0, pw2);
+      };
+      auto issue_a = [&](int s, const RcBlk& b) {
+        uint8_t* dst = L.sA + s * kRcTile;
+        if (b.kind == 0) ptx::tma_load_3d_2sm(dst, &tmH, bar0 + 8 * s, 64 * b.j, 128 * r, b.t, pact);
+        else if (b.kind == 1) ptx::tma_load_3d_2sm(dst, &tmOH, bar0 + 8 * s, 64 * b.j, 128 * r, b.t, pact);
+        else ptx::tma_load_3d_2sm(dst, &tmM, bar0 + 8 * s, (pol.exp & 1) ? 0 : 64 * b.j, 128 * r, b.t, pact);
+      };
+      auto prefetch_w = [&](const RcBlk& b) {
+        if (b.kind == 0) ptx::tma_prefetch_3d(&tmWmh, 64 * b.j, 256 * n1 + 128 * r, 0, pw1);
+        else if (b.kind == 1) ptx::tma_prefetch_3d(&tmXZ, 64 * b.j, 256 * p + 128 * r, 0, pws);
+        else ptx::tma_prefetch_3d(&tmWh, 64 * b.j, 256 * p + 128 * r, 0, pw2);
+      };
+      if (warp == 0) {
+        if (lane == 0)
+          rc_weights(L, T * per, 0, per, leader, pol.pf_dist, tr, dec, issue_w, prefetch_w, (pol.exp & 8) != 0);
+      } else {
+        rc_acts(L, T * per, 0, per, lane, leader, pol.flag_lanes, tr, dec, issue_a, (pol.exp & 4) != 0,
+                (pol.exp & 16) != 0);
       }
     }
   } else if (warp == 1) {
@@ -321,16 +517,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           ptx::mbar_wait(&L.acce[0], (t - 1) & 1);
           ptx::tc_fence_after();
         }
+        tr.step(t, 2);
 #pragma unroll 1
-        for (int i = 0; i < nF1; ++i) rc_consume<false>(L, it++, tmem, i > 0);
+        for (int i = 0; i < nF1; ++i) {
+          rc_consume<false>(L, it++, tmem, i > 0, tr);
+          if (i == 0) tr.step(t, 3);
+        }
         ptx::mma_commit_2sm_mc(&L.accf[0], 0x3);
+        tr.step(t, 4);
         if (t > 0) {
           ptx::mbar_wait(&L.acce[1], (t - 1) & 1);
           ptx::tc_fence_after();
         }
 #pragma unroll 1
-        for (int i = 0; i < 4 + nF2; ++i) rc_consume<false>(L, it++, tmem + 256, i > 0);
+        for (int i = 0; i < 4 + nF2; ++i) {
+          rc_consume<false>(L, it++, tmem + 256, i > 0, tr);
+          if (i == 4) tr.step(t, 5);
+        }
         ptx::mma_commit_2sm_mc(&L.accf[1], 0x3);
+        tr.step(t, 6);
       }
     }
   } else {  // ---------------------------------------------------------------- epilogue warps
@@ -346,21 +551,49 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int cc = 0; cc < 2; ++cc) ld16(n.Crm + (long)b * h + 64 * p + 16 * (grp + 2 * cc), cst + 16 * cc);
 #pragma unroll 1
     for (int t = 0; t < T; ++t) {
+      if (pol.exp & 32) {  // timing experiment: bare epilogue (no reduce, no stores; wrong results)
+        ptx::mbar_wait(&L.accf[0], t & 1);
+        ptx::tc_fence_after();
+        if (tid == 0) {
+          tr.step_tag(t, 1000 + t);
+          tr.step(t, 7);
+        }
+        rc_release_acc(&L.acce[0], leader, lane);
+        rc_publish(&fM[2 * p + r], (uint32_t)(t + 1), tid);
+        if (tid == 0) tr.step(t, 9);
+        ptx::mbar_wait(&L.accf[1], t & 1);
+        ptx::tc_fence_after();
+        if (tid == 0) tr.step(t, 10);
+        rc_release_acc(&L.acce[1], leader, lane);
+        rc_publish(&fH[2 * p + r], (uint32_t)(t + 1), tid);
+        if (tid == 0) tr.step(t, 11);
+        continue;
+      }
       const int byte = n.byte_at(b, t);
       // ---------------------------------------------- F1 epilogue: split-K reduce, m = mx * a
       const float* mxp = n.tab + (long)byte * 5 * h + u1;
-      prefetch_l2(mxp);
+      // this thread's 32 mx values land in its slot of the staging window while the split-K partials
+      // are exchanged (off the critical path; the m staging below uses the window's first half)
+      float* mxs = reinterpret_cast<float*>(w + 4096 + lane * 128);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ptx::cp_async16(mxs + 4 * k, mxp + 4 * k);
       ptx::mbar_wait(&L.accf[0], t & 1);
       ptx::tc_fence_after();
+      if (tid == 0) {
+        tr.step_tag(t, 1000 + t);
+        tr.step(t, 7);
+      }
       float a[32];
       rc_reduce(tmem, 0, gscr + (t & 1) * region, z, q, grp, lane, tid, fP + (n1 * 2 + r) * 4, (uint32_t)(t + 1),
-                &L.acce[0], leader, a);
+                &L.acce[0], leader, a, tr, t, 2);
+      if (tid == 0) tr.step(t, 8);
       {
         float m[32];
+        ptx::cp_async_wait_all();
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           float x[16];
-          ld16(mxp + 16 * g, x);
+          ld16(mxs + 16 * g, x);
 #pragma unroll
           for (int i = 0; i < 16; ++i) m[16 * g + i] = x[i] * a[16 * g + i];
         }
@@ -369,12 +602,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         __syncwarp();
       }
       rc_publish(&fM[2 * p + r], (uint32_t)(t + 1), tid);
+      if (tid == 0) tr.step(t, 9);
       rc_stage_h<2>(w, 80, lane, a);
       warp_rows_out(reinterpret_cast<uint8_t*>(n.Astash + ((long)t * B + b0) * h + u1), 2L * h, w, 80, 64, 32, lane);
       __syncwarp();
       // ---------------------------------------------- F2 epilogue: gates, cell update, hidden state
       ptx::mbar_wait(&L.accf[1], t & 1);
       ptx::tc_fence_after();
+      if (tid == 0) tr.step(t, 10);
       uint32_t gpk[2][32];  // fp16 gate pairs of both chunks (stored after h is published)
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
@@ -406,11 +641,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         rc_stage_h<1>(w + cc * 1536, 48, lane, hv);
       }
       rc_release_acc(&L.acce[1], leader, lane);
+      if (tid == 0) tr.det(t, 6);
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc)
         warp_rows_out(reinterpret_cast<uint8_t*>(n.Hrm + ((long)(t + 1) * B + b0) * h + 64 * p + 16 * (grp + 2 * cc)),
                       2L * h, w + cc * 1536, 48, 32, 32, lane);
+      if (tid == 0) tr.det(t, 7);
       rc_publish(&fH[2 * p + r], (uint32_t)(t + 1), tid);
+      if (tid == 0) tr.step(t, 11);
       // stashes for BPTT: gates (internal order) and c_t
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
@@ -427,6 +665,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                       w + 3072, 80, 64, 32, lane);
       }
       __syncwarp();
+      if (tid == 0) tr.det(t, 8);
     }
   }
   ptx::tc_fence_before();
@@ -445,7 +684,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // Weights are read MN-major straight from the row-major working copies (no transposed copies).
 // Flag values: dZ_s -> T - s, dA_t -> T - t, B1(t) partials -> T - t, B2(t) partials -> T - t + 1.
 // =============================================================================================
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kRcThreads, 1)
     bwd_recur_kernel(const __grid_constant__ CUtensorMap tmDZ, const __grid_constant__ CUtensorMap tmDA,
                      const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmWh,
                      const __grid_constant__ CUtensorMap tmWmh, const __grid_constant__ CUtensorMap tmWdec,
@@ -463,6 +702,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint32_t* fA = flags + 2 * P;   // [P][2]  dA_t chunk p
   uint32_t* fP1 = flags + 4 * P;  // [(n1, r)][4]
   uint32_t* fP2 = flags + 6 * P;  // [(n1, r)][4]
+  __shared__ uint32_t tr_base_s;
+  if (threadIdx.x == 0) tr_base_s = rc_trace_reserve(2 * T + kRcTraceBlk);
   rc_setup(L);
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmDZ);
@@ -476,83 +717,81 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem = *L.tmem_slot;
+  const RcTrace tr{tr_base_s, T, 1 + kRcTraceStep * per, per, 4000};
   const int total = 1 + T * per - (1 + nB2);  // no B2(0)
 
-  if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------------------------ TMA producer
+  if (warp == 0 || warp == kRcActWarp) {
+    {  // ----------------------------------------------------------- TMA producers (weights, activations)
       const uint64_t pact = ptx::make_policy(pol.act), pw1 = ptx::make_policy(pol.w_split),
                      pw2 = ptx::make_policy(pol.w_wide), pws = ptx::make_policy(pol.w_seg);
       const uint32_t bar0 = ptx::mapa_shared(ptx::smem_u32(&L.full[0]), 0);
       // idx -> (t, kind, chunk): kind 0 = B1 dZ chunk, 1 = B2 segment dY_{t-1}, 2 = B2 dA chunk
-      auto decode = [&](int idx, int& t, int& kind, int& j) {
-        if (idx == 0) {  // prologue B2(T): the dY_{T-1} W_dec segment only
-          t = T;
-          kind = 1;
-          j = z;
-          return;
+      auto dec = [&](int u, int i) {
+        RcBlk b;
+        b.flag = nullptr;
+        if (u < 0) {  // prologue B2(T): the dY_{T-1} W_dec segment only
+          b.t = T;
+          b.kind = 1;
+          b.j = z;
+          return b;
         }
-        const int u = (idx - 1) / per, i = (idx - 1) - u * per;
-        t = T - 1 - u;
+        b.t = T - 1 - u;
         if (i < nB1) {
-          kind = 0;
-          j = z * nB1 + (i + n1) % nB1;
+          b.kind = 0;
+          int jj = i + n1 * pol.rotate;
+          if (jj >= nB1) jj -= nB1;
+          b.j = z * nB1 + jj;
+          b.flag = &fZ[2 * (b.j >> 2) + r];
+          b.target = (uint32_t)(T - b.t);
         } else if (i == nB1) {
-          kind = 1;
-          j = z;
+          b.kind = 1;
+          b.j = z;
         } else {
-          kind = 2;
-          j = z * nB2 + (i - nB1 - 1 + n1) % nB2;
+          b.kind = 2;
+          int jj = i - nB1 - 1 + n1 * pol.rotate;
+          if (jj >= nB2) jj -= nB2;
+          b.j = z * nB2 + jj;
+          b.flag = &fA[2 * b.j + r];
+          b.target = (uint32_t)(T - b.t);
+        }
+        return b;
+      };
+      auto issue_w = [&](int s, const RcBlk& b) {
+        uint8_t* dst = L.sB + s * kRcTile;
+        const int u0 = 256 * n1 + 128 * r;  // this CTA's 128 output units (MN-major boxes of 64)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (b.kind == 0) ptx::tma_load_3d_2sm(dst + i * 8192, &tmWh, bar0 + 8 * s, u0 + 64 * i, 64 * b.j, 0, pw2);
+          else if (b.kind == 1)
+            ptx::tma_load_3d_2sm(dst + i * 8192, &tmWdec, bar0 + 8 * s, u0 + 64 * i, 64 * b.j, 0, pws);
+          else ptx::tma_load_3d_2sm(dst + i * 8192, &tmWmh, bar0 + 8 * s, u0 + 64 * i, 64 * b.j, 0, pw1);
         }
       };
-      int wi = 0, ai = 0;
-      uint64_t idle_since = 0;
-#pragma unroll 1
-      while (ai < total) {
-        bool progress = false;
-#pragma unroll 1
-        while (wi < total && wi < ai + kRcStages) {
-          const int s = wi % kRcStages;
-          if (wi >= kRcStages && !ptx::mbar_test(&L.empty[s], ((wi / kRcStages) & 1) ^ 1)) break;
-          int t, kind, j;
-          decode(wi, t, kind, j);
-          if (leader) ptx::mbar_arrive_expect_tx(&L.full[s], 2 * kRcTile);
-          uint8_t* dst = L.sB + s * kRcTile;
-          const int u0 = 256 * n1 + 128 * r;  // this CTA's 128 output units (MN-major boxes of 64)
+      auto issue_a = [&](int s, const RcBlk& b) {
+        uint8_t* dst = L.sA + s * kRcTile;
+        if (b.kind == 0) ptx::tma_load_3d_2sm(dst, &tmDZ, bar0 + 8 * s, 64 * b.j, 128 * r, b.t, pact);
+        else if (b.kind == 1) ptx::tma_load_3d_2sm(dst, &tmDY, bar0 + 8 * s, 64 * b.j, 128 * r, b.t - 1, pact);
+        else ptx::tma_load_3d_2sm(dst, &tmDA, bar0 + 8 * s, 64 * b.j, 128 * r, b.t, pact);
+      };
+      auto prefetch_w = [&](const RcBlk& b) {
+        const int u0 = 256 * n1 + 128 * r;
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            if (kind == 0) ptx::tma_load_3d_2sm(dst + i * 8192, &tmWh, bar0 + 8 * s, u0 + 64 * i, 64 * j, 0, pw2);
-            else if (kind == 1)
-              ptx::tma_load_3d_2sm(dst + i * 8192, &tmWdec, bar0 + 8 * s, u0 + 64 * i, 64 * j, 0, pws);
-            else ptx::tma_load_3d_2sm(dst + i * 8192, &tmWmh, bar0 + 8 * s, u0 + 64 * i, 64 * j, 0, pw1);
-          }
-          ++wi;
-          progress = true;
+        for (int i = 0; i < 2; ++i) {
+          if (b.kind == 0) ptx::tma_prefetch_3d(&tmWh, u0 + 64 * i, 64 * b.j, 0, pw2);
+          else if (b.kind == 1) ptx::tma_prefetch_3d(&tmWdec, u0 + 64 * i, 64 * b.j, 0, pws);
+          else ptx::tma_prefetch_3d(&tmWmh, u0 + 64 * i, 64 * b.j, 0, pw1);
         }
-        if (ai < wi) {
-          int t, kind, j;
-          decode(ai, t, kind, j);
-          bool ready = true;
-          if (kind == 0) ready = ptx::ld_acquire_gpu(&fZ[2 * (j >> 2) + r]) >= (uint32_t)(T - t);
-          else if (kind == 2) ready = ptx::ld_acquire_gpu(&fA[2 * j + r]) >= (uint32_t)(T - t);
-          if (ready) {
-            if (kind != 1) ptx::fence_proxy_async_global();
-            const int s = ai % kRcStages;
-            if (leader) ptx::mbar_arrive_expect_tx(&L.full[s], 2 * kRcTile);
-            uint8_t* dst = L.sA + s * kRcTile;
-            if (kind == 0) ptx::tma_load_3d_2sm(dst, &tmDZ, bar0 + 8 * s, 64 * j, 128 * r, t, pact);
-            else if (kind == 1) ptx::tma_load_3d_2sm(dst, &tmDY, bar0 + 8 * s, 64 * j, 128 * r, t - 1, pact);
-            else ptx::tma_load_3d_2sm(dst, &tmDA, bar0 + 8 * s, 64 * j, 128 * r, t, pact);
-            ++ai;
-            progress = true;
-          }
-        }
-        rc_watchdog(progress, idle_since);
+      };
+      if (warp == 0) {
+        if (lane == 0) rc_weights(L, total, 1, per, leader, pol.pf_dist, tr, dec, issue_w, prefetch_w);
+      } else {
+        rc_acts(L, total, 1, per, lane, leader, pol.flag_lanes, tr, dec, issue_a);
       }
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {  // ------------------------------------------------- MMA issuer
       uint32_t it = 0;
-      rc_consume<true>(L, it++, tmem + 256, false);  // B2(T): dY_{T-1} W_dec
+      rc_consume<true>(L, it++, tmem + 256, false, tr);  // B2(T): dY_{T-1} W_dec
       ptx::mma_commit_2sm_mc(&L.accf[1], 0x3);
 #pragma unroll 1
       for (int u = 0; u < T; ++u) {
@@ -561,15 +800,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           ptx::mbar_wait(&L.acce[0], (u - 1) & 1);
           ptx::tc_fence_after();
         }
+        tr.step(u, 2);
 #pragma unroll 1
-        for (int i = 0; i < nB1; ++i) rc_consume<true>(L, it++, tmem, i > 0);
+        for (int i = 0; i < nB1; ++i) {
+          rc_consume<true>(L, it++, tmem, i > 0, tr);
+          if (i == 0) tr.step(u, 3);
+        }
         ptx::mma_commit_2sm_mc(&L.accf[0], 0x3);
+        tr.step(u, 4);
         if (t == 0) break;
         ptx::mbar_wait(&L.acce[1], u & 1);  // use u of the wide accumulator (use 0 = prologue)
         ptx::tc_fence_after();
 #pragma unroll 1
-        for (int i = 0; i < 1 + nB2; ++i) rc_consume<true>(L, it++, tmem + 256, i > 0);
+        for (int i = 0; i < 1 + nB2; ++i) {
+          rc_consume<true>(L, it++, tmem + 256, i > 0, tr);
+          if (i == 1) tr.step(u, 5);
+        }
         ptx::mma_commit_2sm_mc(&L.accf[1], 0x3);
+        tr.step(u, 6);
       }
     }
   } else {  // ---------------------------------------------------------------- epilogue warps
@@ -596,9 +844,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       prefetch_l2(cp);
       ptx::mbar_wait(&L.accf[1], use & 1);
       ptx::tc_fence_after();
+      if (tid == 0 && t < T) tr.step(T - 1 - t, 10);
       float dh[32];
       rc_reduce(tmem, 256, gscr2 + (t & 1) * region, z, q, grp, lane, tid, fP2 + (n1 * 2 + r) * 4,
-                (uint32_t)(T - t + 1), &L.acce[1], leader, dh);
+                (uint32_t)(T - t + 1), &L.acce[1], leader, dh, tr, t < T ? T - 1 - t : -1, 6);
 #pragma unroll
       for (int g = 0; g < 2; ++g) {  // two groups of 16 units = two 64-column internal chunks
         float gi[16], gf[16], go[16], gu[16], c[16], cpv[16];
@@ -620,12 +869,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           dz[48 + k] = dc * i * (1.f - u * u);                    // dZ_u
           dcs[16 * g + k] = dc * f;                               // dc carry to step s-1
         }
+        if (tid == 0 && t < T && g == 0) tr.det(T - 1 - t, 11);
         rc_stage_h<4>(w, 144, lane, dz);
         warp_rows_out(reinterpret_cast<uint8_t*>(n.G5 + ((long)s * B + b0) * 5 * h + h + (u1 >> 4) * 64 + 64 * g),
                       10L * h, w, 144, 128, 32, lane);
         __syncwarp();
       }
+      if (tid == 0 && t < T) tr.det(T - 1 - t, 10);
       rc_publish(&fZ[2 * p + r], (uint32_t)(T - s), tid);
+      if (tid == 0 && t < T) tr.step(T - 1 - t, 11);
     };
     b2_epi(T, 0);
 #pragma unroll 1
@@ -635,36 +887,43 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int byte = n.byte_at(b, t);
       const float* mxp = n.tab + (long)byte * 5 * h + u1;
       const __half* ap = n.Astash + ((long)t * B + b) * h + u1;
-      prefetch_l2(mxp);
-      prefetch_l2(ap);
+      // mx (32 fp32) and a (32 fp16) of this thread land in the window during the exchange
+      float* mxs = reinterpret_cast<float*>(w + lane * 128);
+      __half* as_ = reinterpret_cast<__half*>(w + 32 * 128 + lane * 64);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ptx::cp_async16(mxs + 4 * k, mxp + 4 * k);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ptx::cp_async16(as_ + 8 * k, ap + 8 * k);
       ptx::mbar_wait(&L.accf[0], u & 1);
       ptx::tc_fence_after();
+      if (tid == 0) {
+        tr.step_tag(u, 2000 + u);
+        tr.step(u, 7);
+      }
       float dm[32];
       rc_reduce(tmem, 0, gscr1 + (t & 1) * region, z, q, grp, lane, tid, fP1 + (n1 * 2 + r) * 4, (uint32_t)(T - t),
-                &L.acce[0], leader, dm);
+                &L.acce[0], leader, dm, tr, u, 2);
+      if (tid == 0) tr.step(u, 8);
       {
-        float da[32];
+        float da[32], dmx[32];
+        ptx::cp_async_wait_all();
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
-          float x[16];
-          ld16(mxp + 16 * g, x);
+          float x[16], av[16];
+          ld16(mxs + 16 * g, x);
+          ld16(as_ + 16 * g, av);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) da[16 * g + i] = dm[16 * g + i] * x[i];
+          for (int i = 0; i < 16; ++i) {
+            da[16 * g + i] = dm[16 * g + i] * x[i];
+            dmx[16 * g + i] = dm[16 * g + i] * av[i];
+          }
         }
+        __syncwarp();  // every lane has read its mx / a slot before the staging below overwrites them
         rc_stage_h<2>(w, 80, lane, da);
         warp_rows_out(reinterpret_cast<uint8_t*>(n.dA + ((long)t * B + b0) * h + u1), 2L * h, w, 80, 64, 32, lane);
         __syncwarp();
-      }
-      if (t > 0) rc_publish(&fA[2 * p + r], (uint32_t)(T - t), tid);
-      {
-        float dmx[32];
-#pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          float av[16];
-          ld16(ap + 16 * g, av);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) dmx[16 * g + i] = dm[16 * g + i] * av[i];
-        }
+        if (t > 0) rc_publish(&fA[2 * p + r], (uint32_t)(T - t), tid);
+        if (tid == 0) tr.step(u, 9);
         rc_stage_h<2>(w, 80, lane, dmx);
         warp_rows_out(reinterpret_cast<uint8_t*>(n.G5 + ((long)t * B + b0) * 5 * h + u1), 10L * h, w, 80, 64, 32,
                       lane);

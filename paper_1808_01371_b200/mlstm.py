@@ -37,7 +37,7 @@ class MlstmConfig(ctypes.Structure):
         ("beta2", ctypes.c_double), ("eps", ctypes.c_double), ("scale_init", ctypes.c_float),
         ("scale_min", ctypes.c_float), ("scale_max", ctypes.c_float),
         ("scale_growth_interval", ctypes.c_int32), ("diverge_patience", ctypes.c_int32),
-        ("reserved0", ctypes.c_int32),
+        ("recurrence", ctypes.c_int32),
     ]
 
 
@@ -109,6 +109,7 @@ _SIGS = {
     "mlstm_loader_destroy": (None, [_vp]),
     "mlstm_last_error": (ctypes.c_char_p, []),
     "mlstm_destroy": (None, [_vp]),
+    "mlstm_sync": (ctypes.c_int, [_vp]),
 }
 
 
@@ -279,6 +280,25 @@ class MLSTM:
         r = mlstm_train_step(self.ctx, bytes_dev.data_ptr(), None if reset_dev is None else reset_dev.data_ptr(),
                              flags)
         return r.as_dict()
+
+    def train_step_async(self, bytes_dev, reset_dev=None):
+        """Enqueues one step with MLSTM_ASYNC; returns the result struct the library fills at the
+        next synchronising call (sync(), or a train_step without the flag)."""
+        assert bytes_dev.dtype.itemsize == 1 and bytes_dev.is_cuda and bytes_dev.is_contiguous()
+        assert tuple(bytes_dev.shape) == (self.B, self.T + 1)
+        out = MlstmStepResult()
+        self._pending = getattr(self, "_pending", []) + [out]  # keeps *out alive until delivered
+        _check(lib().mlstm_train_step(self.ctx, ctypes.c_void_p(bytes_dev.data_ptr()),
+                                      ctypes.c_void_p(0 if reset_dev is None else reset_dev.data_ptr()),
+                                      MLSTM_ASYNC, ctypes.byref(out)))
+        return out
+
+    def sync(self) -> None:
+        """mlstm_sync: delivers every outstanding async result (raises MlstmError on divergence)."""
+        try:
+            _check(lib().mlstm_sync(self.ctx))
+        finally:
+            self._pending = []
 
     def train_step_host(self, bytes_host, reset_host=None) -> dict:
         assert np.asarray(bytes_host).shape == (self.B, self.T + 1)

@@ -5,8 +5,6 @@ The persistent kernels cover 256 rows per micro-batch (one CTA pair along M) and
 256 (h/64 CTA pairs), so these cases use B = 256 with h = 256 (4 pairs, one split-K tile) and
 h = 1024 (16 pairs, four tiles); T = 1 exercises the degenerate window (no recurrent term at all).
 """
-import os
-
 import numpy as np
 import pytest
 
@@ -22,15 +20,7 @@ from gpu_helpers import TOL, compare_grads, inputs, make_model, oracle_step, ora
 
 
 def _model(h, T, recur, **kw):
-    old = os.environ.get("MLSTM_RECUR")
-    os.environ["MLSTM_RECUR"] = "1" if recur else "0"
-    try:
-        return make_model(h, 64, 256, T, "mixed", **kw)
-    finally:
-        if old is None:
-            del os.environ["MLSTM_RECUR"]
-        else:
-            os.environ["MLSTM_RECUR"] = old
+    return make_model(h, 64, 256, T, "mixed", recurrence=1 if recur else 2, **kw)
 
 
 @pytest.mark.parametrize("h,T", [(256, 1), (256, 6), (1024, 5)])

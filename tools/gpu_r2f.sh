@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT"
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_recur.py -x -q > gpurun_out/r2f_tests.log 2>&1
+echo "tests exit $?" >> gpurun_out/r2f_tests.log
+timeout 300 python tools/trace_recur.py > gpurun_out/r2f_trace.log 2>&1
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e >> gpurun_out/r2f_bench.log 2>&1
