@@ -99,6 +99,15 @@ int64_t mlstm_param_count(const mlstm_config* cfg);
  * alive, untouched, until mlstm_destroy.  Returns 0 for an invalid config. */
 size_t mlstm_workspace_bytes(const mlstm_config* cfg);
 
+/* The gradient allreduce's bucket plan for `world` ranks (fp16 SUM of the weight gradients;
+ * SURVEY 8(e)), host only: element ranges of the canonical gradient layout, in the order they are
+ * reduced.  out: host int64 [cap][3] = (offset, count, after) per bucket, after = the work the bucket
+ * waits for: 0 = the first row half of dW_h (units [0, h/2) of every gate; four contiguous ranges),
+ * 1 = dW_h, 2 = dW_mh, 3 = every other gradient (end of the backward).  The buckets tile [0, P) exactly
+ * once.  world == 1, micro-batching or MLSTM_AR_OVERLAP=0: one bucket [0, P) after 3.  *n = number of
+ * buckets; MLSTM_EINVAL if cap < *n (then *n is still set) or the config is invalid. */
+mlstm_status mlstm_allreduce_plan(const mlstm_config* cfg, int32_t world, int64_t* out, int32_t cap, int32_t* n);
+
 /* NCCL unique id for a multi-rank run (NCCL, no parameter server).  Rank 0 calls it
  * and broadcasts the 128 bytes to the other ranks (torch.distributed). */
 mlstm_status mlstm_nccl_unique_id(uint8_t out[128]);
@@ -143,9 +152,12 @@ mlstm_status mlstm_train_step_host(mlstm_ctx* ctx, const uint8_t* bytes_host,
                                    const uint8_t* reset_host, mlstm_step_result* out);
 
 /* Forward-only evaluation of one window of Be <= micro-batch rows from the eval-slot state (state
- * persisted across evaluation minibatches; no update).  bytes: device uint8 [Be][T+1].
- * Outputs (host): nats_sum = global sum of per-position CE (all ranks), tokens = Be*T*world,
- * bpc = nats_sum/tokens*log2(e). */
+ * persisted across evaluation minibatches; no update).  bytes: device uint8 [Be][T+1].  reset: device
+ * uint8 [Be] or NULL: 0 = continue the row's state, 1 = start it from zero, 2 = idle row (state
+ * reset, its positions not counted; the data loader's rows without a shard, mlstm_data.h).
+ * Outputs (host, any may be NULL): nats_sum = global sum of per-position CE (all ranks), tokens =
+ * counted positions (T per row with reset != 2, all ranks), bpc = nats_sum/tokens*log2(e) (0 if no
+ * tokens). */
 mlstm_status mlstm_eval(mlstm_ctx* ctx, const uint8_t* bytes, int32_t Be, const uint8_t* reset,
                         double* nats_sum, int64_t* tokens, double* bpc);
 
@@ -172,9 +184,11 @@ mlstm_status mlstm_get_opt_state(mlstm_ctx* ctx, float* m_out, float* v_out, int
 mlstm_status mlstm_set_opt_state(mlstm_ctx* ctx, const float* m_in, const float* v_in,
                                  int64_t tau, float alpha, int32_t clean_steps, int64_t it);
 
-/* Debug read of an internal buffer of the LAST train step, converted to fp32 on the host.
- * name: "x" (embedded inputs E16[bytes], [T][B][e]), "logits" ([T][B][256]), "h" ([T][B][h]),
- * "c" ([T][B][h]), "loss_rows" (per-position CE [T][B]), "tab" ([256][5h] input-projection table).
+/* Debug read of an internal buffer of the LAST train step (last micro-batch), converted to fp32 on
+ * the host.  name: "m" / "a" (the recurrence's stashes m_t = (W_mx x_t) . a_t and a_t = W_mh h_{t-1},
+ * [T][B][h], as the hot path wrote them), "logits" ([T][B][256]), "h" ([T][B][h]), "c" ([T][B][h]),
+ * "loss_rows" (per-position CE [T][B]), "tab" ([256][5h] input-projection table), "onehot"
+ * ([256][T][B]), "x" (E16[bytes] gathered by a debug-only kernel, [T][B][e]).
  * n: capacity of host_out in floats; MLSTM_EINVAL if too small or name unknown. */
 mlstm_status mlstm_debug_dump(mlstm_ctx* ctx, const char* name, float* host_out, size_t n);
 

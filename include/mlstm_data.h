@@ -41,7 +41,7 @@ void mlstm_corpus_destroy(mlstm_corpus* corpus);
 
 /* Shards of one split: B shards for evaluation (kind MLSTM_SHARDS_EVAL), max(1000, B) for
  * training; the split's records are shuffled with `seed` and dealt round-robin, each shard is the
- * concatenation of its records.  Windows hold T+1 bytes (T inputs + the next byte as the last
+ * concatenation of its records joined with a newline.  Windows hold T+1 bytes (T inputs + the next byte as the last
  * target) and consecutive windows of a row overlap by one byte (Q6).  Fewer records than shards:
  * MLSTM_EINVAL. */
 mlstm_status mlstm_loader_create(const mlstm_corpus* corpus, int32_t split, int32_t kind, int32_t B, int32_t T,
@@ -49,16 +49,29 @@ mlstm_status mlstm_loader_create(const mlstm_corpus* corpus, int32_t split, int3
 int64_t mlstm_loader_num_shards(const mlstm_loader* loader);
 /* Shard i's bytes (test access): copies min(cap, length) bytes to out, length to *len. */
 mlstm_status mlstm_loader_shard(const mlstm_loader* loader, int64_t i, uint8_t* out, int64_t cap, int64_t* len);
-/* The next minibatch: host bytes [B][T+1] and reset [B].  Row j continues its shard from
- * the previous minibatch; when fewer than T+1 bytes remain, row j takes the next unassigned shard
- * (in row order) and reset[j] = 1 (the hidden state restarts at zero at a shard start).  The
- * first minibatch of an epoch has every reset set.  When a row cannot be filled because every shard
- * has been assigned, *end = 1 and the outputs are left untouched (end of epoch, not an error). */
-mlstm_status mlstm_loader_next(mlstm_loader* loader, uint8_t* bytes, uint8_t* reset, int32_t* end);
+/* The next minibatch: host bytes [B][T+1], reset [B] and valid [B] (valid may be NULL).  Row j
+ * continues its shard from the previous minibatch; when fewer than T+1 bytes remain, row j takes the
+ * next unassigned shard (in row order) and reset[j] = 1 (the hidden state restarts at zero at a shard
+ * start).  The first minibatch of an epoch has every reset set.  A row that finds no unassigned
+ * shard idles for the rest of the epoch: valid[j] = 0, zero bytes, reset[j] = 1 (pass reset = 2 for
+ * such rows to mlstm_eval so they are not counted).  When no row is valid -- every shard consumed
+ * (S:347), so every shard byte except a tail shorter than T+1 was an input exactly once -- *end = 1
+ * and the outputs are left untouched (end of epoch, not an error). */
+mlstm_status mlstm_loader_next(mlstm_loader* loader, uint8_t* bytes, uint8_t* reset, uint8_t* valid, int32_t* end);
 /* Back to the start of the epoch: the same shards in the same order ("used for all training epochs
  * with no further shuffling"). */
 mlstm_status mlstm_loader_rewind(mlstm_loader* loader);
 void mlstm_loader_destroy(mlstm_loader* loader);
+
+/* Held-out BPC over one epoch of an evaluation loader, accumulated in the library: rewinds the
+ * loader and runs every minibatch through mlstm_eval from the eval-slot state (reset = the loader's
+ * reset, 2 for idle rows), stopping after max_batches (< 0: the whole epoch).  Outputs (host, any may
+ * be NULL): nats_sum and tokens summed over the batches and all ranks, bpc = nats_sum / tokens / ln 2.
+ * The loader's B and T must equal the context's batch (rows per micro-batch) and seq_len, else
+ * MLSTM_EINVAL.  Collective when world > 1: every rank calls it with loaders yielding equally many
+ * batches. */
+mlstm_status mlstm_heldout_bpc(mlstm_ctx* ctx, mlstm_loader* loader, int64_t max_batches, double* nats_sum,
+                               int64_t* tokens, double* bpc);
 
 #ifdef __cplusplus
 }

@@ -402,11 +402,18 @@ def train_step(st: TrainState, bytes_, lr0=3e-3, decay_iters=100_000, n_global_r
             "alpha": alpha, "lr": lr, "grads": g_unscaled}
 
 
-def evaluate(P: dict, bytes_, h0, c0, reset=None):
-    """Forward-only BPC over one window with persisted state: (nats_sum, tokens, (hT,cT))."""
-    loss_sum, cache, state = forward(P, bytes_, h0, c0, reset=reset)
+def evaluate(P: dict, bytes_, h0, c0, reset=None, valid=None):
+    """Forward-only BPC over one window with persisted state: (nats_sum, tokens, (hT,cT)).
+    Rows with valid[b] == 0 (idle data-loader rows) are not counted; their state restarts at zero."""
     Bn, T1 = np.asarray(bytes_).shape
-    return loss_sum, Bn * (T1 - 1), state
+    if valid is None:
+        loss_sum, cache, state = forward(P, bytes_, h0, c0, reset=reset)
+        return loss_sum, Bn * (T1 - 1), state
+    valid = np.asarray(valid).astype(bool)
+    reset = (np.zeros(Bn, bool) if reset is None else np.asarray(reset).astype(bool)) | ~valid
+    loss_sum, cache, state = forward(P, bytes_, h0, c0, reset=reset)
+    counted = float(np.stack(cache.loss_t, axis=0)[:, valid].sum())
+    return counted, int(valid.sum()) * (T1 - 1), state
 
 
 # --------------------------------------------------------------------------------------

@@ -265,7 +265,8 @@ __global__ void __launch_bounds__(256) ce_kernel(Net<S> n, int Be, float inv_den
     const long r = r0 + lr;
     const int t = r < R ? (int)(r / n.B) : 0;
     const int b = r < R ? (int)(r % n.B) : 0;
-    const bool valid = r < R && b < Be;
+    // evaluation: rows with reset == 2 are idle loader rows (no tokens counted)
+    const bool valid = r < R && b < Be && (with_grad || n.reset[b] != 2);
     float y[8];
     if (valid) {
       const float4 a = reinterpret_cast<const float4*>(n.Y + r * 256)[lane];
@@ -340,6 +341,19 @@ __global__ void __launch_bounds__(256) ce_kernel(Net<S> n, int Be, float inv_den
 // Final fixed-order reductions of the CE partials: block 0 sums the loss partials into
 // st->loss_sum; with_grad: block 1 + v sums column v of the db_dec partials (strided per thread,
 // then a fixed-shape tree: deterministic).  Grid = 1 + 256 * with_grad blocks of 256 threads.
+// Evaluation token count: T positions per row b < Be whose reset flag is not 2 (idle loader rows).
+template <typename S>
+__global__ void eval_tokens_kernel(Net<S> n, int Be, double* tok) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  int mine = 0;
+  for (int b = threadIdx.x; b < Be; b += blockDim.x) mine += n.reset[b] != 2;
+  atomicAdd(&cnt, mine);
+  __syncthreads();
+  if (threadIdx.x == 0) *tok = (double)cnt * n.T;
+}
+
 template <typename S>
 __global__ void __launch_bounds__(256) ce_reduce_kernel(Net<S> n, int nblk, int with_grad) {
   __shared__ double red[256];

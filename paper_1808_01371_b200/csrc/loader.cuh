@@ -94,6 +94,7 @@ mlstm_status mlstm_loader_create(const mlstm_corpus* c, int32_t split, int32_t k
   for (int64_t i = 0; i < (int64_t)idx.size(); ++i) {  // round-robin after the shuffle
     const auto& rec = c->records[idx[i]];
     auto& sh = L->shards[i % nshards];
+    if (!sh.empty()) sh.push_back('\n');  // record boundaries joined with a newline
     sh.insert(sh.end(), rec.begin(), rec.end());
   }
   L->B = B;
@@ -122,28 +123,45 @@ mlstm_status mlstm_loader_rewind(mlstm_loader* L) {
   return MLSTM_OK;
 }
 
-mlstm_status mlstm_loader_next(mlstm_loader* L, uint8_t* bytes, uint8_t* reset, int32_t* end) {
+mlstm_status mlstm_loader_next(mlstm_loader* L, uint8_t* bytes, uint8_t* reset, uint8_t* valid, int32_t* end) {
   if (!L || !bytes || !reset || !end) return fail(MLSTM_EINVAL, "loader_next: null argument");
   const int64_t W = (int64_t)L->T + 1;
   // plan the batch first so that an end of epoch leaves the outputs and cursors untouched
   std::vector<int64_t> sh(L->shard_of), ps(L->pos);
-  std::vector<uint8_t> rs(L->B, 0);
+  std::vector<uint8_t> rs(L->B, 0), ok(L->B, 1);
   int64_t next = L->next_shard;
+  int nvalid = 0;
   for (int j = 0; j < L->B; ++j) {
+    if (sh[j] == -2) {  // this row ran out of shards earlier in the epoch
+      ok[j] = 0;
+      continue;
+    }
     while (sh[j] < 0 || ps[j] + W > (int64_t)L->shards[sh[j]].size()) {  // needs a (new) shard
-      if (next >= (int64_t)L->shards.size()) {
-        *end = 1;
-        return MLSTM_OK;
+      if (next >= (int64_t)L->shards.size()) {  // none left: the row idles for the rest of the epoch
+        sh[j] = -2;
+        ok[j] = 0;
+        break;
       }
       sh[j] = next++;
       ps[j] = 0;
       rs[j] = 1;
     }
+    nvalid += ok[j];
+  }
+  if (nvalid == 0) {  // every shard consumed ("epoch ends when all shards are consumed")
+    *end = 1;
+    return MLSTM_OK;
   }
   for (int j = 0; j < L->B; ++j) {
-    memcpy(bytes + (size_t)j * W, L->shards[sh[j]].data() + ps[j], (size_t)W);
+    if (ok[j]) {
+      memcpy(bytes + (size_t)j * W, L->shards[sh[j]].data() + ps[j], (size_t)W);
+      ps[j] += L->T;  // consecutive windows overlap by one byte (Q6)
+    } else {
+      memset(bytes + (size_t)j * W, 0, (size_t)W);
+      rs[j] = 1;
+    }
     reset[j] = rs[j];
-    ps[j] += L->T;  // consecutive windows overlap by one byte (Q6)
+    if (valid) valid[j] = ok[j];
   }
   L->shard_of = sh;
   L->pos = ps;

@@ -91,6 +91,7 @@ struct mlstm_ctx {
   float *adam_m = nullptr, *adam_v = nullptr;
   uint8_t *bytes = nullptr, *reset = nullptr;
   int32_t* scratch_flag = nullptr;
+  double* eval_tok = nullptr;  // token count of the last mlstm_eval (device, summed over ranks)
   DevState* st = nullptr;
   DevState* st_host = nullptr;  // pinned ring: slots [0, kAsyncRing) for MLSTM_ASYNC steps, slot kAsyncRing for
                                 // synchronous ones (each step copies its DevState into its own slot)
@@ -324,6 +325,7 @@ void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
   n.st = cv.take<DevState>(1);
   c->st = n.st;
   c->scratch_flag = cv.take<int32_t>(4);
+  c->eval_tok = cv.take<double>(2);
 }
 
 mlstm_status validate(const mlstm_config* cfg) {
@@ -1101,6 +1103,39 @@ bool wh_split_ok(mlstm_ctx* c) {
   return p.pair && p.splits == 1;
 }
 
+// The gradient allreduce's buckets as element ranges of the canonical fp16 arena,
+// in the order they are reduced, each tagged with the event it waits for: kAfterWhA = the first half of
+// dW_h (internal rows [0, 2h) = units [0, h/2) of every gate: four contiguous canonical ranges),
+// kAfterWh = dW_h, kAfterWmh = dW_mh, kAfterA = the end of graph A (E, W_mx, W_x, biases, W_dec: the
+// per-byte sums, db and the decoder gradient).  Without overlap (world 1, micro-batches, or
+// MLSTM_AR_OVERLAP=0): one range, the whole arena, after graph A.
+enum { kAfterWhA = 0, kAfterWh = 1, kAfterWmh = 2, kAfterA = 3 };
+struct ArRange {
+  int64_t off, count;
+  int32_t after;
+};
+std::vector<ArRange> allreduce_plan(mlstm_ctx* c) {
+  std::vector<ArRange> r;
+  const ParamOffsets& po = c->po;
+  if (!c->overlap_now()) {
+    r.push_back({0, c->P, kAfterA});
+    return r;
+  }
+  const long hh = c->h;
+  if (wh_split_ok<__half>(c)) {
+    for (int half = 0; half < 2; ++half)
+      for (int g = 0; g < 4; ++g)
+        r.push_back({po.Wh + ((long)g * hh + half * (hh / 2)) * hh, (hh / 2) * hh, half == 0 ? kAfterWhA : kAfterWh});
+  } else {
+    r.push_back({po.Wh, po.b - po.Wh, kAfterWh});
+  }
+  r.push_back({po.Wmh, po.Wx - po.Wmh, kAfterWmh});
+  r.push_back({0, po.Wmh, kAfterA});
+  r.push_back({po.Wx, po.Wh - po.Wx, kAfterA});
+  r.push_back({po.b, po.P - po.b, kAfterA});
+  return r;
+}
+
 // One step: for each micro-batch, copy its rows of the input (host or device) into the step
 // buffers and run graph A (forward, BPTT, weight gradients, fp32 accumulation across micro-batches);
 // then the allreduce and graph B (overflow check, scaler, Adam, cast) once.
@@ -1128,35 +1163,23 @@ mlstm_status run_train(mlstm_ctx* c, const uint8_t* bytes, const uint8_t* reset,
     c->cur_phase = PH_ALLREDUCE;
     const ncclDataType_t dt = c->mixed ? ncclFloat16 : ncclFloat32;
     if (c->overlap_now()) {
-      // fp16 SUM in three buckets on the comm stream; bucket k waits for the GEMM that wrote it
-      const ParamOffsets& po = c->po;
+      // fp16 SUM in buckets on the comm stream (allreduce_plan); each group of buckets waits for the
+      // GEMM that wrote it, the last group carries the loss sum
       S* a = n.arena;
       cudaStream_t cs = c->comm_stream;
       CUDA_OR_FAIL(c, cudaEventRecord(c->ev_a_end, c->stream));
-      const long hh = c->h;
-      const bool split_wh = wh_split_ok<S>(c);
-      for (int half = split_wh ? 0 : 1; half < 2; ++half) {  // W_h: units [0, h/2) then [h/2, h) of each gate
-        CUDA_OR_FAIL(c, cudaStreamWaitEvent(cs, half == 0 ? c->ev_wh_a : c->ev_wh, 0));
-        if (!split_wh) {
-          NCCL_OR_FAIL(c, ncclAllReduce(a + po.Wh, a + po.Wh, (size_t)(po.b - po.Wh), dt, ncclSum, c->comm, cs));
-          break;
-        }
+      const cudaEvent_t after_ev[4] = {c->ev_wh_a, c->ev_wh, c->ev_wmh, c->ev_a_end};
+      const std::vector<ArRange> plan = allreduce_plan(c);
+      for (size_t k = 0; k < plan.size();) {
+        const int32_t after = plan[k].after;
+        CUDA_OR_FAIL(c, cudaStreamWaitEvent(cs, after_ev[after], 0));
         NCCL_OR_FAIL(c, ncclGroupStart());
-        for (int g = 0; g < 4; ++g) {
-          S* p0 = a + po.Wh + ((long)g * hh + half * (hh / 2)) * hh;
-          NCCL_OR_FAIL(c, ncclAllReduce(p0, p0, (size_t)(hh / 2) * hh, dt, ncclSum, c->comm, cs));
-        }
+        for (; k < plan.size() && plan[k].after == after; ++k)
+          NCCL_OR_FAIL(c, ncclAllReduce(a + plan[k].off, a + plan[k].off, (size_t)plan[k].count, dt, ncclSum, c->comm, cs));
+        if (k == plan.size())
+          NCCL_OR_FAIL(c, ncclAllReduce(&c->st->loss_sum, &c->st->loss_sum, 1, ncclFloat64, ncclSum, c->comm, cs));
         NCCL_OR_FAIL(c, ncclGroupEnd());
       }
-      CUDA_OR_FAIL(c, cudaStreamWaitEvent(cs, c->ev_wmh, 0));
-      NCCL_OR_FAIL(c, ncclAllReduce(a + po.Wmh, a + po.Wmh, (size_t)(po.Wx - po.Wmh), dt, ncclSum, c->comm, cs));
-      CUDA_OR_FAIL(c, cudaStreamWaitEvent(cs, c->ev_a_end, 0));
-      NCCL_OR_FAIL(c, ncclGroupStart());
-      NCCL_OR_FAIL(c, ncclAllReduce(a, a, (size_t)po.Wmh, dt, ncclSum, c->comm, cs));
-      NCCL_OR_FAIL(c, ncclAllReduce(a + po.Wx, a + po.Wx, (size_t)(po.Wh - po.Wx), dt, ncclSum, c->comm, cs));
-      NCCL_OR_FAIL(c, ncclAllReduce(a + po.b, a + po.b, (size_t)(po.P - po.b), dt, ncclSum, c->comm, cs));
-      NCCL_OR_FAIL(c, ncclAllReduce(&c->st->loss_sum, &c->st->loss_sum, 1, ncclFloat64, ncclSum, c->comm, cs));
-      NCCL_OR_FAIL(c, ncclGroupEnd());
       CUDA_OR_FAIL(c, cudaEventRecord(c->ev_comm, cs));
       CUDA_OR_FAIL(c, cudaStreamWaitEvent(c->stream, c->ev_comm, 0));
     } else {
@@ -1228,7 +1251,7 @@ mlstm_status after_step(mlstm_ctx* c, mlstm_step_result* out) {
 }
 
 template <typename S>
-mlstm_status run_eval(mlstm_ctx* c, int Be, double* nats) {
+mlstm_status run_eval(mlstm_ctx* c, int Be, double* nats, double* tok) {
   Net<S>& n = net<S>(c);
   g_force_plan = c->force_plan;
   const mlstm_status fs = enqueue_forward<S>(c, MLSTM_SLOT_EVAL);
@@ -1236,12 +1259,28 @@ mlstm_status run_eval(mlstm_ctx* c, int Be, double* nats) {
   RET_IF(fs);
   LAUNCH(c, (ce_kernel<S><<<c->nblk_ce, 256, 0, c->stream>>>(n, Be, 0.f, 0)));
   LAUNCH(c, (ce_reduce_kernel<S><<<1, 256, 0, c->stream>>>(n, c->nblk_ce, 0)));
+  LAUNCH(c, (eval_tokens_kernel<S><<<1, 256, 0, c->stream>>>(n, Be, c->eval_tok)));
   LAUNCH(c, (state_out_kernel<S><<<grid_for((long)c->B * c->h), 256, 0, c->stream>>>(n, MLSTM_SLOT_EVAL)));
-  if (c->world > 1)
+  if (c->world > 1) {
     NCCL_OR_FAIL(c, ncclAllReduce(&c->st->loss_sum, &c->st->loss_sum, 1, ncclFloat64, ncclSum, c->comm, c->stream));
+    NCCL_OR_FAIL(c, ncclAllReduce(c->eval_tok, c->eval_tok, 1, ncclFloat64, ncclSum, c->comm, c->stream));
+  }
   CUDA_OR_FAIL(c, cudaMemcpyAsync(nats, &c->st->loss_sum, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(tok, c->eval_tok, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
   return MLSTM_OK;
+}
+
+// One evaluation window from device (D2D) or host (H2D) buffers; nats and tokens over all ranks.
+mlstm_status eval_window(mlstm_ctx* c, const uint8_t* bytes, int32_t Be, const uint8_t* reset, cudaMemcpyKind kind,
+                         double* nats, double* tok) {
+  CUDA_OR_FAIL(c, cudaMemsetAsync(c->bytes, 0, (size_t)c->B * (c->T + 1), c->stream));
+  CUDA_OR_FAIL(c, cudaMemcpyAsync(c->bytes, bytes, (size_t)Be * (c->T + 1), kind, c->stream));
+  CUDA_OR_FAIL(c, cudaMemsetAsync(c->reset, 0, c->B, c->stream));
+  if (reset) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->reset, reset, Be, kind, c->stream));
+  set_microbatch_kernel<<<1, 1, 0, c->stream>>>(c->st, 0);
+  CUDA_OR_FAIL(c, cudaGetLastError());
+  return c->mixed ? run_eval<__half>(c, Be, nats, tok) : run_eval<float>(c, Be, nats, tok);
 }
 
 float half_bits_to_float(uint16_t b) {
@@ -1323,6 +1362,23 @@ size_t mlstm_workspace_bytes(const mlstm_config* cfg) {
   mlstm_ctx tmp;
   set_dims(&tmp, cfg);
   return layout_bytes(&tmp);
+}
+
+mlstm_status mlstm_allreduce_plan(const mlstm_config* cfg, int32_t world, int64_t* out, int32_t cap, int32_t* n) {
+  RET_IF(validate(cfg));
+  if (world < 1 || !n || (cap > 0 && !out)) return fail(MLSTM_EINVAL, "bad arguments");
+  mlstm_ctx tmp;
+  set_dims(&tmp, cfg);
+  tmp.world = world;
+  const std::vector<ArRange> plan = allreduce_plan(&tmp);
+  *n = (int32_t)plan.size();
+  if ((int32_t)plan.size() > cap) return fail(MLSTM_EINVAL, "cap smaller than the number of buckets");
+  for (size_t k = 0; k < plan.size(); ++k) {
+    out[3 * k] = plan[k].off;
+    out[3 * k + 1] = plan[k].count;
+    out[3 * k + 2] = plan[k].after;
+  }
+  return MLSTM_OK;
 }
 
 mlstm_status mlstm_nccl_unique_id(uint8_t out[128]) {
@@ -1461,18 +1517,11 @@ mlstm_status mlstm_eval(mlstm_ctx* c, const uint8_t* bytes, int32_t Be, const ui
                         int64_t* tokens, double* bpc) {
   RET_IF(ctx_ok(c));
   if (!bytes || Be <= 0 || Be > c->B) return fail(MLSTM_EINVAL, "eval needs bytes and 0 < Be <= batch");
-  CUDA_OR_FAIL(c, cudaMemsetAsync(c->bytes, 0, (size_t)c->B * (c->T + 1), c->stream));
-  CUDA_OR_FAIL(c, cudaMemcpyAsync(c->bytes, bytes, (size_t)Be * (c->T + 1), cudaMemcpyDeviceToDevice, c->stream));
-  CUDA_OR_FAIL(c, cudaMemsetAsync(c->reset, 0, c->B, c->stream));
-  if (reset) CUDA_OR_FAIL(c, cudaMemcpyAsync(c->reset, reset, Be, cudaMemcpyDeviceToDevice, c->stream));
-  set_microbatch_kernel<<<1, 1, 0, c->stream>>>(c->st, 0);
-  CUDA_OR_FAIL(c, cudaGetLastError());
-  double nats = 0;
-  RET_IF(c->mixed ? run_eval<__half>(c, Be, &nats) : run_eval<float>(c, Be, &nats));
-  const int64_t tok = (int64_t)Be * c->T * c->world;
+  double nats = 0, tok = 0;
+  RET_IF(eval_window(c, bytes, Be, reset, cudaMemcpyDeviceToDevice, &nats, &tok));
   if (nats_sum) *nats_sum = nats;
-  if (tokens) *tokens = tok;
-  if (bpc) *bpc = nats / (double)tok / std::log(2.0);
+  if (tokens) *tokens = (int64_t)tok;
+  if (bpc) *bpc = tok > 0 ? nats / tok / std::log(2.0) : 0.0;
   return MLSTM_OK;
 }
 
@@ -1614,6 +1663,13 @@ mlstm_status mlstm_debug_dump(mlstm_ctx* c, const char* name, float* host_out, s
     CUDA_OR_FAIL(c, cudaMemcpyAsync(host_out, src, cnt * 4, cudaMemcpyDeviceToHost, c->stream));
     CUDA_OR_FAIL(c, cudaStreamSynchronize(c->stream));
     return MLSTM_OK;
+  }
+  if (nm == "m" || nm == "a") {  // the stashes the recurrence wrote: m_t = mx_t * a_t and a_t, [T][B][h]
+    const long cnt = T * B * h;
+    if (!need(cnt)) return fail(MLSTM_EINVAL, "buffer too small");
+    const void* src = nm == "m" ? (c->mixed ? (const void*)c->nh.Mrm : (const void*)c->nf.Mrm)
+                                : (c->mixed ? (const void*)c->nh.Astash : (const void*)c->nf.Astash);
+    return read_floats(c, src, cnt, host_out);
   }
   if (nm == "h") {
     const long cnt = T * B * h;
@@ -1803,3 +1859,33 @@ void mlstm_destroy(mlstm_ctx* c) {
 }  // extern "C"
 
 #include "loader.cuh"
+
+extern "C" {
+
+mlstm_status mlstm_heldout_bpc(mlstm_ctx* c, mlstm_loader* L, int64_t max_batches, double* nats_sum, int64_t* tokens,
+                               double* bpc) {
+  RET_IF(ctx_ok(c));
+  if (!L) return fail(MLSTM_EINVAL, "null loader");
+  if (L->B != c->B || L->T != c->T) return fail(MLSTM_EINVAL, "loader B / T differ from the context's batch / seq_len");
+  RET_IF(mlstm_loader_rewind(L));
+  const size_t W = (size_t)c->T + 1;
+  std::vector<uint8_t> by((size_t)c->B * W), rs(c->B), ok(c->B);
+  double nats = 0, tok = 0;
+  for (int64_t k = 0; max_batches < 0 || k < max_batches; ++k) {
+    int32_t end = 0;
+    RET_IF(mlstm_loader_next(L, by.data(), rs.data(), ok.data(), &end));
+    if (end) break;
+    for (int b = 0; b < c->B; ++b)
+      if (!ok[b]) rs[b] = 2;  // idle row: state reset, no tokens
+    double n = 0, t = 0;
+    RET_IF(eval_window(c, by.data(), c->B, rs.data(), cudaMemcpyHostToDevice, &n, &t));
+    nats += n;
+    tok += t;
+  }
+  if (nats_sum) *nats_sum = nats;
+  if (tokens) *tokens = (int64_t)tok;
+  if (bpc) *bpc = tok > 0 ? nats / tok / std::log(2.0) : 0.0;
+  return MLSTM_OK;
+}
+
+}  // extern "C"

@@ -104,12 +104,14 @@ _SIGS = {
                                            ctypes.c_uint64, _P(ctypes.c_void_p)]),
     "mlstm_loader_num_shards": (ctypes.c_int64, [_vp]),
     "mlstm_loader_shard": (ctypes.c_int, [_vp, ctypes.c_int64, _u8p, ctypes.c_int64, _P(ctypes.c_int64)]),
-    "mlstm_loader_next": (ctypes.c_int, [_vp, _u8p, _u8p, _i32p]),
+    "mlstm_loader_next": (ctypes.c_int, [_vp, _u8p, _u8p, _u8p, _i32p]),
+    "mlstm_heldout_bpc": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _dp, _i64p, _dp]),
     "mlstm_loader_rewind": (ctypes.c_int, [_vp]),
     "mlstm_loader_destroy": (None, [_vp]),
     "mlstm_last_error": (ctypes.c_char_p, []),
     "mlstm_destroy": (None, [_vp]),
     "mlstm_sync": (ctypes.c_int, [_vp]),
+    "mlstm_allreduce_plan": (ctypes.c_int, [_P(MlstmConfig), ctypes.c_int32, _i64p, ctypes.c_int32, _i32p]),
 }
 
 
@@ -170,6 +172,14 @@ def mlstm_workspace_bytes(cfg: MlstmConfig) -> int:
     if n == 0:
         raise MlstmError(MLSTM_EINVAL, lib().mlstm_last_error().decode())
     return n
+
+
+def mlstm_allreduce_plan(cfg: MlstmConfig, world: int) -> list[tuple[int, int, int]]:
+    """Bucket plan of the gradient allreduce: [(offset, count, after)] in reduction order."""
+    n = ctypes.c_int32()
+    out = np.zeros((16, 3), dtype=np.int64)
+    _check(lib().mlstm_allreduce_plan(ctypes.byref(cfg), world, out.ctypes.data_as(_i64p), 16, ctypes.byref(n)))
+    return [tuple(int(v) for v in row) for row in out[: n.value]]
 
 
 def mlstm_nccl_unique_id() -> bytes:
@@ -435,11 +445,14 @@ class Loader:
         return buf[:n.value].tobytes()
 
     def next(self):
+        """(bytes [B, T+1], reset [B], valid [B]) or None at the end of the epoch."""
         by = np.zeros((self.B, self.T + 1), dtype=np.uint8)
         rs = np.zeros(self.B, dtype=np.uint8)
+        ok = np.zeros(self.B, dtype=np.uint8)
         end = ctypes.c_int32()
-        _check(lib().mlstm_loader_next(self.h, _ptr(by, ctypes.c_uint8), _ptr(rs, ctypes.c_uint8), ctypes.byref(end)))
-        return None if end.value else (by, rs)
+        _check(lib().mlstm_loader_next(self.h, _ptr(by, ctypes.c_uint8), _ptr(rs, ctypes.c_uint8),
+                                       _ptr(ok, ctypes.c_uint8), ctypes.byref(end)))
+        return None if end.value else (by, rs, ok)
 
     def rewind(self):
         _check(lib().mlstm_loader_rewind(self.h))
@@ -460,18 +473,12 @@ class Loader:
 
 
 def heldout_bpc(model, loader: Loader, max_batches: int | None = None) -> float:
-    """Held-out BPC over one epoch of an evaluation loader: every window through mlstm_eval
-    with the loader's reset masks (state persisted within a shard, zero at a shard start)."""
-    import torch
-    nats = tokens = 0
-    loader.rewind()
-    for k, (by, rs) in enumerate(loader):
-        if max_batches is not None and k >= max_batches:
-            break
-        n, tok, _ = model.eval(torch.from_numpy(by).cuda(), torch.from_numpy(rs).cuda())
-        nats += n
-        tokens += tok
-    return nats / tokens / math.log(2.0)
+    """Held-out BPC over one epoch of an evaluation loader: mlstm_heldout_bpc (the library runs
+    every window through the evaluation forward with the loader's reset masks and accumulates)."""
+    nats, tok, bpc = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
+    _check(lib().mlstm_heldout_bpc(model.ctx, loader.h, -1 if max_batches is None else max_batches,
+                                   ctypes.byref(nats), ctypes.byref(tok), ctypes.byref(bpc)))
+    return bpc.value
 
 
 def cell_features(model, texts):

@@ -38,42 +38,60 @@ def test_shard_counts(kind, B, count):
     recs = _records(2100, 1)
     sh = D.make_shards(recs, B, kind, seed=3)
     assert len(sh) == count
-    assert sum(len(s) for s in sh) == sum(len(r) for r in recs)       # every record in exactly one shard
+    # every record in exactly one shard, records joined by one newline each
+    assert sum(len(s) for s in sh) == sum(len(r) for r in recs) + len(recs) - count
     with pytest.raises(ValueError):
         D.make_shards(recs[:10], 16, "eval", 0)
+
+
+def test_records_joined_with_newline():
+    """S:363 "Record boundaries inside a shard are joined with a newline delimiter": a one-shard split
+    of three records is their newline-joined concatenation in the seeded round-robin order."""
+    recs = [b"ab", b"cde", b"f"]
+    order = D.seeded_shuffle(list(range(3)), 4)
+    assert D.make_shards(recs, 1, "eval", seed=4) == [b"\n".join(recs[i] for i in order)]
 
 
 def test_tiny_minibatch_enumeration():
     """S:345 (windows of T+1 bytes overlapping by one byte, Q6): shards 'abcdefghi', 'jklmnopqr', B=2,
     T=4 -> batch 1 rows ('abcde', 'jklmn') with reset on both, batch 2 ('efghi', 'nopqr') without."""
     out = list(D.minibatches([b"abcdefghi", b"jklmnopqr"], B=2, T=4))
-    assert out == [([b"abcde", b"jklmn"], [1, 1]), ([b"efghi", b"nopqr"], [0, 0])]
+    assert out == [([b"abcde", b"jklmn"], [1, 1], [1, 1]), ([b"efghi", b"nopqr"], [0, 0], [1, 1])]
     # B=1, one shard -> sequential windows (S:346)
     assert [r[0][0] for r in D.minibatches([b"0123456789"], B=1, T=3)] == [b"0123", b"3456", b"6789"]
+    # S:347 "epoch ends when all shards are consumed": with three shards and two rows, row 0 takes the
+    # third shard after its first and the epoch runs on with row 1 idle until that shard is done
+    out = list(D.minibatches([b"abcde", b"fghij", b"klmnopqrs"], B=2, T=4))
+    assert [o[0][0] for o in out] == [b"abcde", b"klmno", b"opqrs"]
+    assert [o[2] for o in out] == [[1, 1], [1, 0], [1, 0]]
+    assert [o[1] for o in out] == [[1, 1], [1, 1], [0, 1]]
 
 
 def test_contiguity_coverage_and_target_alignment():
-    """S:350-353: each row's consecutive windows are contiguous ranges of one shard (until a reset);
-    every byte of a finished shard but its tail (< T+1 bytes) is an input exactly once (the epoch
-    ends when a row finds no unassigned shard; the other rows' open shards end there, Q25)."""
+    """each row's consecutive windows are contiguous ranges of one shard (until a reset), and
+    over one epoch every shard byte but its tail (< T+1 bytes) is an input exactly once."""
     shards = D.make_shards(_records(1500, 2, 50, 400), 4, "eval", seed=1)
     B, T = 4, 16
     seen = {i: [] for i in range(len(shards))}
     cur = [None] * B
     nxt = 0
-    for rows, reset in D.minibatches(shards, B, T):
+    for rows, reset, valid in D.minibatches(shards, B, T):
         for j in range(B):
+            if not valid[j]:
+                assert rows[j] == bytes(T + 1) and reset[j] == 1
+                continue
             if reset[j]:
                 cur[j] = nxt
                 nxt += 1
             seen[cur[j]].append(rows[j])
+    assert nxt == len(shards)  # every shard was taken
     for i, wins in seen.items():
         s = shards[i]
-        # reconstruction: windows overlap by one byte and tile a prefix of the shard
+        # reconstruction: windows overlap by one byte and tile a prefix of the shard; the rest is a
+        # tail shorter than one window
         recon = wins[0] + b"".join(w[1:] for w in wins[1:]) if wins else b""
         assert s.startswith(recon)
-        # only the rows' shards still open when the epoch ended keep more than a tail
-        assert len(s) - len(recon) < T + 1 or i in cur
+        assert len(s) - len(recon) < T + 1 if wins else len(s) < T + 1
 
 
 # ---------------------------------------------------------------- library vs oracle ------
@@ -95,14 +113,16 @@ def test_library_loader_matches_oracle(B, T, kind, seed):
     for i in (0, 1, len(shards) - 1):
         assert L.shard(i) == shards[i]
     n = 0
-    for (rows, reset), got in zip(D.minibatches(shards, B, T), L):
-        assert got[0].tobytes() == b"".join(rows) and got[1].tolist() == reset
+    for (rows, reset, valid), got in zip(D.minibatches(shards, B, T), L):
+        assert got[0].tobytes() == b"".join(rows) and got[1].tolist() == reset and got[2].tolist() == valid
         n += 1
         if n == 400:
             break
+    if n < 400:  # both ended the epoch at the same batch
+        assert L.next() is None
     L.rewind()                                                           # same shards, same order
     first = L.next()
-    rows, reset = next(iter(D.minibatches(shards, B, T)))
+    rows, reset, valid = next(iter(D.minibatches(shards, B, T)))
     assert first[0].tobytes() == b"".join(rows) and first[1].tolist() == reset
 
 

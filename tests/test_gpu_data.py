@@ -30,9 +30,9 @@ def test_heldout_bpc_matches_oracle(precision, tol):
     P = O.unflatten(oracle_theta(h, e), h, e)
     hs, cs = np.zeros((B, h)), np.zeros((B, h))
     nats = tokens = 0.0
-    for rows, reset in D.minibatches(D.make_shards(va, B, "eval", seed + 1), B, T):
+    for rows, reset, valid in D.minibatches(D.make_shards(va, B, "eval", seed + 1), B, T):
         by = np.frombuffer(b"".join(rows), dtype=np.uint8).reshape(B, T + 1)
-        n, tok, (hs, cs) = O.evaluate(P, by, hs, cs, reset=np.array(reset))
+        n, tok, (hs, cs) = O.evaluate(P, by, hs, cs, reset=np.array(reset), valid=np.array(valid))
         nats += n
         tokens += tok
     ref = nats / tokens / np.log(2.0)

@@ -51,3 +51,25 @@ def test_8192d_sampled_row_losses():
     assert np.abs(got - want).max() < 2e-2, np.abs(got - want).max()
     rel = np.abs(got.mean(0) - want.mean(0)) / want.mean(0)
     assert rel.max() < 5e-3, rel
+
+
+@pytest.mark.parametrize("h,B,T,recurrence", [(4096, 16, 16, 0), (4096, 256, 6, 1), (8192, 16, 8, 0)])
+def test_full_width_mixed_gradients(h, B, T, recurrence):
+    """All 8 gradients of one mixed step at the paper's widths (C3's h=4096; C5's h=8192) against the fp64
+    oracle on the same parameters and bytes: cosine >= 0.999 per tensor, loss within rel 5e-3 (north_star
+    tolerances).  The window is short so the oracle's fp64 BPTT at these widths stays in the tens of
+    seconds; recurrence=1 runs the persistent dataflow kernels at their 256-row shape."""
+    from gpu_helpers import TOL, compare_grads, oracle_step
+    e = 64
+    m = make_model(h, e, B, T, "mixed", recurrence=recurrence)
+    assert m.uses_recur() == (recurrence == 1)
+    theta = oracle_theta(h, e)
+    by = inputs(B, T)
+    r = m.train_step(to_dev(by))
+    assert np.isfinite(r["loss_nats"]) and not r["skipped"]
+    loss_ref, g_ref, _, _ = oracle_step(theta, by, h, e)
+    assert abs(r["loss_nats"] - loss_ref) / loss_ref <= TOL["mixed"]["loss_rel"], (r["loss_nats"], loss_ref)
+    rep = compare_grads(m.get_grads().astype(np.float64), g_ref, h, e, "mixed")
+    for n, v in rep.items():
+        assert v >= TOL["mixed"]["grad_cos"], (n, v, rep)
+    m.close()

@@ -125,6 +125,42 @@ def test_byte_indexing_bit_exact(precision):
     assert np.array_equal(x, Ew[by[:, :T].T])
 
 
+@pytest.mark.parametrize("precision,recurrence", [("fp32", 0), ("mixed", 0), ("mixed", 1)])
+def test_hot_path_gather_of_mx(precision, recurrence):
+    """The byte gather the hot path performs (P:36 m = (W_mx x_t) . (W_mh h_{t-1}); x_t = E[s_t]): the
+    m_t and a_t rows the recurrence stashed, against (i) the oracle's m_t, a_t on the same parameters,
+    bytes and carried state, and (ii) the table row of the byte at (b, t): in fp32 mode m_t is exactly
+    tab[s_t, :h] * a_t (one fp32 multiply), so a wrong byte, row or unit fails bit for bit."""
+    h, e = (64, 64) if recurrence == 0 else (256, 64)
+    B, T = (6, 5) if recurrence == 0 else (256, 3)
+    m = make_model(h, e, B, T, precision, recurrence=recurrence)
+    assert m.uses_recur() == (recurrence == 1)
+    theta0 = oracle_theta(h, e)
+    rng = np.random.default_rng(5)
+    h0 = rng.uniform(-0.9, 0.9, (B, h)).astype(np.float32)
+    c0 = rng.uniform(-1.0, 1.0, (B, h)).astype(np.float32)
+    if precision == "mixed":
+        h0 = h0.astype(np.float16).astype(np.float32)
+    m.set_state(h0, c0)
+    by = inputs(B, T, kind="uniform")
+    m.train_step(to_dev(by))
+    mm = m.debug_dump("m", T * B * h).reshape(T, B, h).astype(np.float64)
+    aa = m.debug_dump("a", T * B * h).reshape(T, B, h).astype(np.float64)
+    tab = m.debug_dump("tab", 256 * 5 * h).reshape(256, 5 * h)
+    _, cache, _ = O.forward(split(theta0, h, e), by, h0.astype(np.float64), c0.astype(np.float64))
+    tol = 1e-5 if precision == "fp32" else 2e-2
+    for t in range(T):
+        ref_a, ref_m = cache.a[t], cache.m[t]
+        assert np.abs(aa[t] - ref_a).max() <= tol * max(1.0, np.abs(ref_a).max()), t
+        assert np.abs(mm[t] - ref_m).max() <= tol * max(1.0, np.abs(ref_m).max()), t
+    mx = tab[by[:, :T].T, :h].astype(np.float64)  # [T][B][h]: the table row of each input byte
+    if precision == "fp32":
+        assert np.array_equal(mm.astype(np.float32), (mx.astype(np.float32) * aa.astype(np.float32)))
+    else:  # m rounded to fp16 from fp32 a; a itself stored in fp16
+        assert np.abs(mm - mx * aa).max() <= 2e-3 * max(1.0, np.abs(mm).max())
+    m.close()
+
+
 def test_overflow_predicate_bit_exact():
     m = make_model(64, 64, 4, 4, "mixed")
     rng = np.random.default_rng(0)
@@ -164,6 +200,65 @@ def test_loss_scale_overflow_decisions_and_replay():
     m2 = make_model(h, e, B, T, "mixed")
     m2.set_opt_state(alpha=1.0)
     assert m2.train_step(to_dev(inputs(B, T)))["skipped"] == 0
+
+
+def test_long_scaler_replay_with_injected_overflows():
+    """64 steps with overflows injected at random steps (W_dec scaled by 1e9 for that step only:
+    the fp16 gradients overflow at any alpha >= 1).  Every injected step is skipped with the parameters
+    untouched, and the GPU's alpha trace equals the oracle scaler (reading Q9) replayed on the
+    GPU's own skip flags, growth every 3 clean steps included."""
+    h, e, B, T = 64, 64, 4, 16
+    m = make_model(h, e, B, T, "mixed", scale_growth_interval=3, scale_init=2.0 ** 10, scale_max=2.0 ** 24)
+    st = O.ScalerState(alpha=2.0 ** 10, growth_interval=3, alpha_max=2.0 ** 24)
+    rng = np.random.default_rng(7)
+    flags = rng.random(64) < 0.3
+    n_skipped = 0
+    for k, inject in enumerate(flags):
+        good = m.get_params()
+        if inject:
+            bad = split(good, h, e)
+            bad["W_dec"] = bad["W_dec"] * 1e9
+            m.set_params(O.flatten(bad))
+        r = m.train_step(to_dev(inputs(B, T, k=k)))
+        assert r["loss_scale"] == st.alpha, (k, r["loss_scale"], st.alpha)
+        if inject:
+            assert r["skipped"] == 1, k
+            m.set_params(good)  # the skipped step left the masters untouched: restore the unscaled decoder
+        if r["skipped"]:
+            assert np.array_equal(m.get_params(), good)
+        n_skipped += r["skipped"]
+        _, st = O.scaler_step(st, bool(r["skipped"]))
+        assert m.get_opt_state()["alpha"] == st.alpha, k
+    assert n_skipped >= flags.sum()
+
+
+@pytest.mark.parametrize("precision", ["fp32", "mixed"])
+def test_loss_scale_invariance(precision):
+    """the unscaled gradients do not depend on alpha while nothing under- or overflows.  Scaling
+    by a power of two is exact in binary floating point, so in fp32 mode alpha = 1 and alpha = 2^10
+    give bitwise-identical unscaled gradients.  In mixed mode alpha = 2^8 and 2^12 agree to cosine
+    1 - 1e-5 per tensor, while alpha = 1 loses the small fp16 gradients to underflow -- the reason the
+    paper scales the loss -- and is measurably further from the fp64 oracle than alpha = 2^10."""
+    h, e, B, T = 128, 64, 8, 12
+    alphas = (1.0, 2.0 ** 10) if precision == "fp32" else (1.0, 2.0 ** 8, 2.0 ** 10, 2.0 ** 12)
+    grads = {}
+    for alpha in alphas:
+        m = make_model(h, e, B, T, precision)
+        m.set_opt_state(alpha=alpha)
+        r = m.train_step(to_dev(inputs(B, T)))
+        assert r["loss_scale"] == alpha and not r["skipped"]
+        grads[alpha] = m.get_grads().astype(np.float64)
+        m.close()
+    if precision == "fp32":
+        assert np.array_equal(grads[1.0], grads[2.0 ** 10])
+        return
+    rep = compare_grads(grads[2.0 ** 12], grads[2.0 ** 8], h, e, "mixed")
+    assert min(rep.values()) >= 0.99999, rep
+    _, g_ref, _, _ = oracle_step(oracle_theta(h, e), inputs(B, T), h, e)
+    lo = compare_grads(grads[1.0], g_ref, h, e, "mixed")
+    hi = compare_grads(grads[2.0 ** 10], g_ref, h, e, "mixed")
+    assert min(hi.values()) >= TOL["mixed"]["grad_cos"], hi
+    assert min(hi.values()) > min(lo.values()), (lo, hi)
 
 
 @pytest.mark.parametrize("alpha", [1.0, 2.0 ** 24, 2.0 ** 40])
