@@ -39,8 +39,11 @@ CONFIGS = {
                                "dynamic loss scaling"),
     "C4": (4096, 64, 4096, 256, "large batch: mLSTM h=4096 e=64, seq 256, 4096 rows/GPU as 4 x 1024-row "
                                 "micro-batches (global batch 32768 at 8 GPUs), fp16/fp32 mixed"),
-    "C5": (8192, 64, 128, 256, "8192-d mLSTM e=64, seq 256, batch 128/GPU, fp16/fp32 mixed"),
+    "C5": (8192, 64, 128, 256, "8192-d mLSTM e=64, seq 256, batch 128/GPU, fp16/fp32 mixed, lr0 7.8e-4 (P:240)"),
+    "C5-256": (8192, 64, 256, 256, "8192-d mLSTM e=64, seq 256, batch 256/GPU (P:240's memory-bound 96/GPU on "
+                                   "V100; B200 fits 256 without recompute), fp16/fp32 mixed, lr0 7.8e-4"),
 }
+LR0 = {"C5": 7.8e-4, "C5-256": 7.8e-4}  # the 8192-d model's square-root-scaled learning rate
 MICRO_BATCH = {"C4": 1024}
 DEVSTATE_BYTES = 56  # the device scalar block the step copies back (loss, alpha, lr, skip, it, tau)
 
@@ -279,6 +282,8 @@ def main():
     cfg = M.mlstm_default_config(hidden=h, embed=e, batch=B, seq_len=T, precision=M.MLSTM_MIXED,
                                  micro_batch=MICRO_BATCH.get(args.config, 0),
                                  weight_norm=1 if args.weight_norm else 0, recurrence=args.recurrence)
+    if args.config in LR0:
+        cfg.lr0 = LR0[args.config]
     nid = None
     if world > 1:
         t = torch.zeros(128, dtype=torch.uint8, device="cuda")

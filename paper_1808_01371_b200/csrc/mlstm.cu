@@ -695,7 +695,8 @@ RcPolicy recur_policy(mlstm_ctx* c) {
   // the per-timestep activation chunks are re-read by every pair within microseconds (normal); the
   // split GEMM's weight (W_mh, 2h^2 bytes) and the segment operands (XZT / W_dec) are re-read every
   // timestep (evict_last); W_h (8h^2 bytes, more than L2) streams (evict_first unless MLSTM_L2_WH)
-  return RcPolicy{0u, pol_last(1.f), c->l2_wh > 0 ? pol_last(c->l2_wh) : kPolFirst, pol_last(1.f), c->rc_flag_lanes, c->rc_pf_dist, c->rc_rotate, c->rc_exp};
+  const uint32_t wide = getenv("MLSTM_RC_WNORMAL") ? 0u : (c->l2_wh > 0 ? pol_last(c->l2_wh) : kPolFirst);
+  return RcPolicy{0u, pol_last(1.f), wide, pol_last(1.f), c->rc_flag_lanes, c->rc_pf_dist, c->rc_rotate, c->rc_exp};
 }
 
 mlstm_status launch_fwd_recur(mlstm_ctx* c) {

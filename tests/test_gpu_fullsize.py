@@ -73,3 +73,34 @@ def test_full_width_mixed_gradients(h, B, T, recurrence):
     for n, v in rep.items():
         assert v >= TOL["mixed"]["grad_cos"], (n, v, rep)
     m.close()
+
+
+def test_8192d_256_rows_sampled_row_losses():
+    """8192-d at 256 rows per GPU (P:240 trained it at 96 rows/GPU 'due to memory constraints' on V100;
+    the stash of 256 rows fits a B200 without recompute): the launch configuration of bench.py's
+    C5-256 line on a T=16 window, sampled rows against the fp64 oracle."""
+    h, e, B, T = 8192, 64, 256, 16
+    r, got, want = sampled_row_losses(h, e, B, T, 0, [0, 200, 255])
+    assert np.isfinite(r["loss_nats"]) and not r["skipped"]
+    assert np.abs(got - want).max() < 2e-2, np.abs(got - want).max()
+    rel = np.abs(got.mean(0) - want.mean(0)) / want.mean(0)
+    assert rel.max() < 5e-3, rel
+
+
+def test_8192d_three_step_mixed_trace_at_paper_lr():
+    """Three mixed-precision steps of the 8192-d model at the paper's 8192-d learning rate (7.8e-4)
+    against the fp64 oracle loop (mixed-mode overflow decision): losses within the north_star bound
+    at every step, the same skip decisions and loss scale, and the parameter updates aligned."""
+    from gpu_helpers import TOL, cosine
+    h, e, B, T = 8192, 64, 16, 8
+    m = make_model(h, e, B, T, "mixed", lr0=7.8e-4)
+    st = O.new_train_state(h, e, B, seed=0x5EED)
+    for k in range(3):
+        by = inputs(B, T, k=k)
+        r = m.train_step(to_dev(by))
+        ro = O.train_step(st, by, lr0=7.8e-4, precision="mixed")
+        assert abs(r["loss_nats"] - ro["loss_nats"]) <= TOL["mixed"]["loss_rel"] * ro["loss_nats"], (k, r, ro)
+        assert bool(r["skipped"]) == ro["skipped"] and r["loss_scale"] == ro["alpha"], (k, r, ro)
+    theta0 = oracle_theta(h, e)
+    assert cosine(m.get_params().astype(np.float64) - theta0, st.theta - theta0) > 0.99
+    m.close()

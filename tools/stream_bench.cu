@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(384, 1) stream_bench(const __grid_constant__ C
 // rc_acts, rc_consume): the difference to stream_bench isolates their overheads.
 __global__ void __launch_bounds__(kRcThreads, 1) lib_core(const __grid_constant__ CUtensorMap tA,
                                                           const __grid_constant__ CUtensorMap tB, int iters,
-                                                          unsigned long long* out) {
+                                                          unsigned long long* out, int storm, uint32_t* flag) {
   extern __shared__ uint8_t smem_raw[];
   const RcLayout L(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -167,7 +167,12 @@ __global__ void __launch_bounds__(kRcThreads, 1) lib_core(const __grid_constant_
     out[2 * p] = t0;
     out[2 * p + 1] = ptx::globaltimer();
   }
-  if (warp >= 2 && warp < kRcActWarp) ptx::mbar_wait(&L.accf[0], 0);
+  if (warp >= 2 && warp < kRcActWarp) {
+    if (storm && warp == 2 && lane == 0) {  // an epilogue thread spinning on an acquire flag (CCTL.IVALL)
+      while (!ptx::mbar_test(&L.accf[0], 0)) (void)ptx::ld_acquire_gpu(flag);
+    }
+    ptx::mbar_wait(&L.accf[0], 0);
+  }
   ptx::tc_fence_before();
   ptx::cluster_sync();
   if (warp == 1) {
@@ -238,29 +243,36 @@ int main() {
                  maps ? ", alternating maps" : "");
         printf("%-52s %10.3f\n", name, us / cfg.iters);
       }
-  {
-    cudaFuncSetAttribute(lib_core, cudaFuncAttributeMaxDynamicSharedMemorySize, kRcSmem);
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(128);
-    lc.blockDim = dim3(kRcThreads);
-    lc.dynamicSmemBytes = kRcSmem;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    for (int rep = 0; rep < 2; ++rep) cudaLaunchKernelEx(&lc, lib_core, ta, tb, 4096, d);
-    cudaError_t e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) {
-      printf("lib_core error %s\n", cudaGetErrorString(e));
-      return 1;
+  uint32_t* flag;
+  cudaMalloc(&flag, 4);
+  cudaMemset(flag, 0, 4);
+  for (int storm : {0, 1})
+    for (int smem_kb : {200, 226}) {
+      const int sm = smem_kb * 1024 < kRcSmem ? kRcSmem : smem_kb * 1024;
+      cudaFuncSetAttribute(lib_core, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(128);
+      lc.blockDim = dim3(kRcThreads);
+      lc.dynamicSmemBytes = sm;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      for (int rep = 0; rep < 2; ++rep) cudaLaunchKernelEx(&lc, lib_core, ta, tb, 4096, d, storm, flag);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) {
+        printf("lib_core error %s\n", cudaGetErrorString(e));
+        return 1;
+      }
+      cudaMemcpy(h.data(), d, 2 * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+      double us = 0;
+      for (int p = 0; p < 64; ++p) us += (double)(h[2 * p + 1] - h[2 * p]) / 1e3;
+      char name[128];
+      snprintf(name, sizeof name, "library core, %d KB smem%s", sm / 1024, storm ? ", acquire-spinning thread" : "");
+      printf("%-52s %10.3f\n", name, us / 64 / 4096);
     }
-    cudaMemcpy(h.data(), d, 2 * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-    double us = 0;
-    for (int p = 0; p < 64; ++p) us += (double)(h[2 * p + 1] - h[2 * p]) / 1e3;
-    printf("%-52s %10.3f\n", "library producers + rc_consume (recur.cuh)", us / 64 / 4096);
-  }
   return 0;
 }
