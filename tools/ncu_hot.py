@@ -13,8 +13,18 @@ for w in ["gpu__time_duration.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_pe
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 hdr = rows[1]
-data = [dict(zip(hdr, x)) for x in rows[2:] if len(x) == len(hdr)]
 key = "Warp Stall Sampling (All Samples)"
+
+
+def _num(v):
+    try:
+        return float(v or 0)
+    except ValueError:
+        return None
+
+
+data = [dict(zip(hdr, x)) for x in rows[2:] if len(x) == len(hdr)]
+data = [d for d in data if key in d and _num(d[key]) is not None]
 tot = sum(float(d[key] or 0) for d in data)
 for d in sorted(data, key=lambda d: -float(d[key] or 0))[:n]:
     print(f"{float(d[key]) / tot * 100:5.1f}%  {d['Source'][:100]}  exec={d['Instructions Executed']}")
