@@ -133,11 +133,13 @@ struct RcLayout {
 };
 
 // Flag words (reset to 0 before each launch), P = pairs:
-//   [0, 2P)   chunk flags X[p][r]  (fwd: H_t of pair p;  bwd: dZ_s of pair p)
+//   [0, 2P)   chunk flags X[p][r]  (fwd: H_t of pair p;  bwd: unused)
 //   [2P, 4P)  chunk flags Y[p][r]  (fwd: M_t chunk p;   bwd: dA_t chunk p)
 //   [4P, 6P)  split partial flags of the first N = h GEMM  [(n1, r)][z]  (fwd F1, bwd B1)
 //   [6P, 8P)  split partial flags of the second            [(n1, r)][z]  (bwd B2)
-constexpr int kRcFlagWords(int P) { return 8 * P; }
+//   [8P, 16P) bwd: dZ_s chunk flags [(p, r)][c], c = the pair's 64-column chunk (16 units x 4 gates),
+//             published per chunk so B1 starts on the first chunks while the rest are computed
+constexpr int kRcFlagWords(int P) { return 16 * P; }
 // Split-K scratch: per (GEMM, timestep parity) region, per (tile n1, rank r) group
 // [zsrc 4][zdst 4][16 float4 column groups][128 rows].  Alternating parities keep a fast CTA's next
 // partial from overwriting one a slow peer has not read yet (the flags order t before t + 2).
@@ -698,10 +700,10 @@ __global__ void __launch_bounds__(kRcThreads, 1)
   const int n1 = p >> 2, z = p & 3;
   const int h = n.h, B = n.B, T = n.T;
   const int nB1 = h / 64, nB2 = h / 256, per = nB1 + 1 + nB2;
-  uint32_t* fZ = flags;           // [P][2]  dZ_s of units [64p, +64)
   uint32_t* fA = flags + 2 * P;   // [P][2]  dA_t chunk p
   uint32_t* fP1 = flags + 4 * P;  // [(n1, r)][4]
   uint32_t* fP2 = flags + 6 * P;  // [(n1, r)][4]
+  uint32_t* fZc = flags + 8 * P;  // [(p, r)][4 chunks]
   __shared__ uint32_t tr_base_s;
   if (threadIdx.x == 0) tr_base_s = rc_trace_reserve(2 * T + kRcTraceBlk);
   rc_setup(L);
@@ -737,11 +739,14 @@ __global__ void __launch_bounds__(kRcThreads, 1)
         }
         b.t = T - 1 - u;
         if (i < nB1) {
+          // the K range's 64-column dZ chunks: first the ones each producer publishes first (its c = 0, 2
+          // chunks, written by the first pass of the gate backward), then the c = 1, 3 ones
           b.kind = 0;
-          int jj = i + n1 * pol.rotate;
-          if (jj >= nB1) jj -= nB1;
-          b.j = z * nB1 + jj;
-          b.flag = &fZ[2 * (b.j >> 2) + r];
+          const int half = i >= (nB1 >> 1), ii = i - half * (nB1 >> 1);
+          int pp = (ii >> 1) + n1 * pol.rotate;  // producer pair within the K range (nB1 / 4 of them)
+          if (pp >= (nB1 >> 2)) pp -= nB1 >> 2;
+          b.j = z * nB1 + 4 * pp + 2 * (ii & 1) + half;
+          b.flag = &fZc[((b.j >> 2) * 2 + r) * 4 + (b.j & 3)];
           b.target = (uint32_t)(T - b.t);
         } else if (i == nB1) {
           b.kind = 1;
@@ -832,6 +837,7 @@ __global__ void __launch_bounds__(kRcThreads, 1)
 #pragma unroll
     for (int i = 0; i < 32; ++i) dcs[i] = 0.f;
     // B2(t) epilogue: dH of step s = t - 1 -> gate backward -> dZ_s, dc
+    float ccar[32];  // c_s of the next gate backward: this one's c_{s-1}, carried in registers
     auto b2_epi = [&](int t, int use) {
       const int s = t - 1;
       const long BH = (long)B * h;
@@ -840,7 +846,7 @@ __global__ void __launch_bounds__(kRcThreads, 1)
       const float* cp = n.Crm + (long)s * BH + (long)b * h + u1;
       prefetch_l2(gates);
       prefetch_l2(gates + 64);
-      prefetch_l2(cs);
+      if (t == T) prefetch_l2(cs);
       prefetch_l2(cp);
       ptx::mbar_wait(&L.accf[1], use & 1);
       ptx::tc_fence_after();
@@ -848,19 +854,22 @@ __global__ void __launch_bounds__(kRcThreads, 1)
       float dh[32];
       rc_reduce(tmem, 256, gscr2 + (t & 1) * region, z, q, grp, lane, tid, fP2 + (n1 * 2 + r) * 4,
                 (uint32_t)(T - t + 1), &L.acce[1], leader, dh, tr, t < T ? T - 1 - t : -1, 6);
+      if (t == T) {
+        ld16(cs, ccar);
+        ld16(cs + 16, ccar + 16);
+      }
 #pragma unroll
       for (int g = 0; g < 2; ++g) {  // two groups of 16 units = two 64-column internal chunks
-        float gi[16], gf[16], go[16], gu[16], c[16], cpv[16];
+        float gi[16], gf[16], go[16], gu[16], cpv[16];
         ld16(gates + 64 * g, gi);
         ld16(gates + 64 * g + 16, gf);
         ld16(gates + 64 * g + 32, go);
         ld16(gates + 64 * g + 48, gu);
-        ld16(cs + 16 * g, c);
         ld16(cp + 16 * g, cpv);
         float dz[64];
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          const float kk = act_tanh<__half>(c[k]);
+          const float kk = act_tanh<__half>(ccar[16 * g + k]);
           const float i = gi[k], f = gf[k], o = go[k], u = gu[k], d = dh[16 * g + k];
           dz[32 + k] = d * kk * o * (1.f - o);                    // dZ_o
           const float dc = dcs[16 * g + k] + d * o * (1.f - kk * kk);
@@ -868,16 +877,25 @@ __global__ void __launch_bounds__(kRcThreads, 1)
           dz[16 + k] = dc * cpv[k] * f * (1.f - f);               // dZ_f
           dz[48 + k] = dc * i * (1.f - u * u);                    // dZ_u
           dcs[16 * g + k] = dc * f;                               // dc carry to step s-1
+          ccar[16 * g + k] = cpv[k];                              // c_{s-1} is the next step's c_s
         }
         if (tid == 0 && t < T && g == 0) tr.det(T - 1 - t, 11);
         rc_stage_h<4>(w, 144, lane, dz);
         warp_rows_out(reinterpret_cast<uint8_t*>(n.G5 + ((long)s * B + b0) * 5 * h + h + (u1 >> 4) * 64 + 64 * g),
                       10L * h, w, 144, 128, 32, lane);
         __syncwarp();
+        // chunk c = 2 grp + g (all 128 rows of this rank) is complete once the four warps of this
+        // group stored it: publish it on its own flag (B1 of the next timestep may start on it)
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + grp) : "memory");
+        if (warp == 2 + 4 * grp && lane == 0) {
+          ptx::fence_acq_rel_gpu();
+          ptx::st_relaxed_gpu(&fZc[(p * 2 + r) * 4 + 2 * grp + g], (uint32_t)(T - s));
+        }
       }
-      if (tid == 0 && t < T) tr.det(T - 1 - t, 10);
-      rc_publish(&fZ[2 * p + r], (uint32_t)(T - s), tid);
-      if (tid == 0 && t < T) tr.step(T - 1 - t, 11);
+      if (tid == 0 && t < T) {
+        tr.det(T - 1 - t, 10);
+        tr.step(T - 1 - t, 11);
+      }
     };
     b2_epi(T, 0);
 #pragma unroll 1
