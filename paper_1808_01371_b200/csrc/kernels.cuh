@@ -117,8 +117,17 @@ __global__ void wn_grad_kernel(Net<S> n) {
     for (int j = lane; j < len; j += 32) dot = fmaf(to_f(n.arena[off + j]), n.master[off + j], dot);
     const float nrm = n.wn_norm[r];
     const float dg = warp_sum(dot) / nrm, sc = n.master[gi] / nrm, k = dg / nrm;
-    for (int j = lane; j < len; j += 32) n.arena[off + j] = to_s<S>(sc * (to_f(n.arena[off + j]) - k * n.master[off + j]));
-    if (lane == 0) n.arena[gi] = to_s<S>(dg);
+    bool bad = false;
+    for (int j = lane; j < len; j += 32) {
+      const float gv = sc * (to_f(n.arena[off + j]) - k * n.master[off + j]);
+      n.arena[off + j] = to_s<S>(gv);
+      bad |= s_nonfinite<S>(gv);
+    }
+    if (lane == 0) {
+      n.arena[gi] = to_s<S>(dg);
+      bad |= s_nonfinite<S>(dg);
+    }
+    if (bad) n.st->overflow = 1;
   }
 }
 
@@ -227,8 +236,12 @@ __global__ void grad_accum_kernel(Net<S> n) {
   const bool first = mb == 0, last = mb == n.nmb - 1;
   for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n.po.P; q += (long)gridDim.x * blockDim.x) {
     const float g = (first ? 0.f : n.gacc[q]) + to_f(n.arena[q]);
-    if (last) n.arena[q] = to_s<S>(g);
-    else n.gacc[q] = g;
+    if (last) {
+      n.arena[q] = to_s<S>(g);
+      if (s_nonfinite<S>(g)) n.st->overflow = 1;
+    } else {
+      n.gacc[q] = g;
+    }
   }
 }
 
@@ -372,7 +385,10 @@ __global__ void __launch_bounds__(256) ce_reduce_kernel(Net<S> n, int nblk, int 
   }
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) n.st->loss_sum = (n.st->mb == 0 ? 0.0 : n.st->loss_sum) + red[0];
-    else n.arena[n.po.bdec + blockIdx.x - 1] = to_s<S>((float)red[0]);
+    else {
+      n.arena[n.po.bdec + blockIdx.x - 1] = to_s<S>((float)red[0]);
+      if (s_nonfinite<S>((float)red[0])) n.st->overflow = 1;
+    }
   }
 }
 
@@ -420,6 +436,10 @@ struct EpiWgrad {
     S* dst = n.arena + off + r * N + col0;
 #pragma unroll
     for (int q = 0; q < NG; ++q) st16(dst + 16 * q, v + 16 * q);
+    bool bad = false;  // overflow predicate at the writer (the separate scan runs only when world > 1)
+#pragma unroll
+    for (int i = 0; i < 16 * NG; ++i) bad |= s_nonfinite<S>(v[i]);
+    if (bad) n.st->overflow = 1;
   }
 };
 
@@ -436,6 +456,7 @@ __global__ void wgrad_finalize_kernel(Net<S> n, const float* __restrict__ part, 
     } else {
       const long r = (mode == 1) ? canon_of_int(row, n.h) : row;
       n.arena[off + r * N + col] = to_s<S>(s);
+      if (s_nonfinite<S>(s)) n.st->overflow = 1;
     }
   }
 }
@@ -515,6 +536,7 @@ __global__ void seg_finalize_kernel(Net<S> n, const float* __restrict__ part, in
     if (MODE == 0) dst = n.po.E + i;
     else dst = (r < n.h) ? n.po.Wmx + (long)r * n.e + c : n.po.Wx + (long)(r - n.h) * n.e + c;
     n.arena[dst] = to_s<S>(s);
+    if (s_nonfinite<S>(s)) n.st->overflow = 1;
   }
 }
 
@@ -526,6 +548,7 @@ __global__ void db_kernel(Net<S> n) {
     float s = 0.f;
     for (int v = 0; v < 256; ++v) s += n.Scan[(long)v * 5 * h + h + r];
     n.arena[n.po.b + r] = to_s<S>(s);
+    if (s_nonfinite<S>(s)) n.st->overflow = 1;
   }
 }
 

@@ -1037,7 +1037,11 @@ mlstm_status enqueue_train_b(mlstm_ctx* c) {
   const mlstm_config& cf = c->cfg;
   phase(c, PH_OPT);
   if (c->po.wn) LAUNCH(c, (wn_grad_kernel<S><<<grid_for(10L * c->h * 32), 256, 0, c->stream>>>(n)));
-  LAUNCH(c, (overflow_kernel<S><<<grid_for(c->P), 256, 0, c->stream>>>(n.arena, c->P, &c->st->overflow)));
+  // overflow predicate: with one rank every writer of the gradient arena already flagged a
+  // non-finite fp16 value; after a SUM allreduce finite values can still overflow, so the reduced
+  // buffer (identical on every rank) is scanned
+  if (c->world > 1)
+    LAUNCH(c, (overflow_kernel<S><<<grid_for(c->P), 256, 0, c->stream>>>(n.arena, c->P, &c->st->overflow)));
   LAUNCH(c, (adam_kernel<S><<<grid_for(c->P), 256, 0, c->stream>>>(n, c->adam_m, c->adam_v, (float)cf.beta1,
                                                                    (float)cf.beta2, (float)cf.eps, cf.lr0,
                                                                    (long)cf.decay_iters)));

@@ -128,6 +128,18 @@ template <>
 __device__ __forceinline__ float to_s<float>(float x) {
   return x;
 }
+// Whether the fp32 value v is non-finite once stored as S (the overflow predicate of P:126 applied at
+// the writer): binary16 RNE sends |v| >= 65520 to inf (65504 is the largest finite), NaN stays NaN.
+template <typename S>
+__device__ __forceinline__ bool s_nonfinite(float v);
+template <>
+__device__ __forceinline__ bool s_nonfinite<__half>(float v) {
+  return !(fabsf(v) < 65520.f);
+}
+template <>
+__device__ __forceinline__ bool s_nonfinite<float>(float v) {
+  return !(fabsf(v) <= 3.402823466e38f);
+}
 __device__ __forceinline__ float to_f(__half x) { return __half2float(x); }
 __device__ __forceinline__ float to_f(float x) { return x; }
 
