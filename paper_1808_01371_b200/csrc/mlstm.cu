@@ -127,6 +127,7 @@ struct mlstm_ctx {
   // persistent dataflow recurrence (recur.cuh): mlstm_config.recurrence = 1 (or MLSTM_RECUR=1)
   int recur_env = 1;
   int recur_ok = -1;
+  int rc_wkm = 0;                 // MLSTM_RC_WKM=1: persistent BPTT reads the transposed (K-major) weights
   int rc_exp = 0;                 // MLSTM_RC_EXP: timing experiments (wrong results), see RcPolicy
   int rc_rotate = 1;              // MLSTM_RC_ROTATE
   int rc_pf_dist = 0;             // MLSTM_RC_PF: weight k-blocks prefetched into L2 ahead of the ring
@@ -373,6 +374,7 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   if (const char* v = getenv("MLSTM_BWD_PERSIST")) c->bwd_persist = v[0] != '0';
   if (const char* v = getenv("MLSTM_RECUR")) c->recur_env = atoi(v);
   if (const char* v = getenv("MLSTM_RC_EXP")) c->rc_exp = atoi(v);
+  if (const char* v = getenv("MLSTM_RC_WKM")) c->rc_wkm = atoi(v) != 0;
   if (const char* v = getenv("MLSTM_RC_ROTATE")) c->rc_rotate = atoi(v) != 0;
   if (const char* v = getenv("MLSTM_RC_PF")) c->rc_pf_dist = std::max(0, atoi(v));
   if (const char* v = getenv("MLSTM_RC_FLAG_LANES")) c->rc_flag_lanes = std::max(1, std::min(32, atoi(v)));
@@ -672,7 +674,8 @@ bool recur_on(mlstm_ctx* c) {
   if (c->recur_ok >= 0) return c->recur_ok != 0;
   c->recur_ok = 0;
   if (!recur_shape_ok(c) || !c->rc_scratch) return false;
-  for (const void* kern : {(const void*)fwd_recur_kernel, (const void*)bwd_recur_kernel}) {
+  for (const void* kern : {(const void*)fwd_recur_kernel, (const void*)bwd_recur_kernel<false>,
+                           (const void*)bwd_recur_kernel<true>}) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kRcSmem) != cudaSuccess) {
       cudaGetLastError();
       return false;
@@ -729,12 +732,17 @@ mlstm_status launch_bwd_recur(mlstm_ctx* c) {
   const Opd dZ{n.G5 + h, B, 4L * h, 5L * h, T, 5L * B * h};
   const Opd dA{n.dA, B, h, h, T, (long)B * h};
   const Opd dY{n.dY, B, 256, 256, T, (long)B * 256};
-  // weights MN-major straight from the row-major working copies: element (unit n, k) at k*h + n
-  const Opd Wh{n.Wh_w, h, 4L * h, h, 1, 4L * h * h, 0, true, true};
-  const Opd Wmh{n.Wmh_w, h, h, h, 1, (long)h * h, 0, true, true};
-  const Opd Wdec{n.Wdec_w, h, 256, h, 1, 256L * h, 0, true, true};
-  const CUtensorMap *mZ = get_map(c, dZ, 128), *mA = get_map(c, dA, 128), *mY = get_map(c, dY, 128),
-                    *mW2 = get_map(c, Wh, 64), *mW1 = get_map(c, Wmh, 64), *mD = get_map(c, Wdec, 64);
+  const CUtensorMap *mZ = get_map(c, dZ, 128), *mA = get_map(c, dA, 128), *mY = get_map(c, dY, 128);
+  const CUtensorMap *mW2, *mW1, *mD;
+  if (c->rc_wkm) {  // K-major from the transposed working copies (element (unit n, k) at n * K + k)
+    mW2 = get_map(c, Opd{n.WhT, h, 4L * h, 4L * h, 1, 4L * h * h}, 128);
+    mW1 = get_map(c, Opd{n.WmhT, h, h, h, 1, (long)h * h}, 128);
+    mD = get_map(c, Opd{n.WdecT, h, 256, 256, 1, 256L * h}, 128);
+  } else {  // MN-major straight from the row-major working copies: element (unit n, k) at k*h + n
+    mW2 = get_map(c, Opd{n.Wh_w, h, 4L * h, h, 1, 4L * h * h, 0, true, true}, 64);
+    mW1 = get_map(c, Opd{n.Wmh_w, h, h, h, 1, (long)h * h, 0, true, true}, 64);
+    mD = get_map(c, Opd{n.Wdec_w, h, 256, h, 1, 256L * h, 0, true, true}, 64);
+  }
   if (!mZ || !mA || !mY || !mW2 || !mW1 || !mD) {
     c->failed = MLSTM_ECUDA;
     return MLSTM_ECUDA;
@@ -742,8 +750,12 @@ mlstm_status launch_bwd_recur(mlstm_ctx* c) {
   CUDA_OR_FAIL(c, cudaMemsetAsync(c->rc_flags, 0, sizeof(uint32_t) * kRcFlagWords(h / 64), c->stream));
   cudaLaunchAttribute at[2];
   cudaLaunchConfig_t cfg = recur_cfg(c, at, true);
-  CUDA_OR_FAIL(c, cudaLaunchKernelEx(&cfg, bwd_recur_kernel, *mZ, *mA, *mY, *mW2, *mW1, *mD, n, c->rc_scratch,
-                                     c->rc_flags, recur_policy(c)));
+  if (c->rc_wkm)
+    CUDA_OR_FAIL(c, cudaLaunchKernelEx(&cfg, bwd_recur_kernel<true>, *mZ, *mA, *mY, *mW2, *mW1, *mD, n, c->rc_scratch,
+                                       c->rc_flags, recur_policy(c)));
+  else
+    CUDA_OR_FAIL(c, cudaLaunchKernelEx(&cfg, bwd_recur_kernel<false>, *mZ, *mA, *mY, *mW2, *mW1, *mD, n, c->rc_scratch,
+                                       c->rc_flags, recur_policy(c)));
   count_launch(c);
   return MLSTM_OK;
 }
@@ -755,7 +767,7 @@ mlstm_status enqueue_transposes(mlstm_ctx* c) {
   const int h = c->h;
   dim3 blk(32, 8);
   if constexpr (std::is_same<S, __half>::value) {  // h is a multiple of 64
-    if (recur_on(c)) return MLSTM_OK;  // the persistent backward reads W_h, W_mh, W_dec MN-major
+    if (recur_on(c) && !c->rc_wkm) return MLSTM_OK;  // the persistent backward reads W_h, W_mh, W_dec MN-major
     LAUNCH(c, (transpose64_kernel<<<dim3(h / 64, h / 64), blk, 0, c->stream>>>(n.Wmh_w, n.WmhT, h, h)));
     LAUNCH(c, (transpose64_kernel<<<dim3(h / 64, 4 * h / 64), blk, 0, c->stream>>>(n.Wh_w, n.WhT, 4 * h, h)));
     LAUNCH(c, (transpose64_kernel<<<dim3(h / 64, 256 / 64), blk, 0, c->stream>>>(n.Wdec_w, n.WdecT, 256, h)));

@@ -686,6 +686,9 @@ __global__ void __launch_bounds__(kRcThreads, 1)
 // Weights are read MN-major straight from the row-major working copies (no transposed copies).
 // Flag values: dZ_s -> T - s, dA_t -> T - t, B1(t) partials -> T - t, B2(t) partials -> T - t + 1.
 // =============================================================================================
+// WKM: the weights come K-major from the transposed working copies (one 128-row TMA box per stage)
+// instead of MN-major from the row-major ones (two 64 x 64 boxes per stage; no transposes needed).
+template <bool WKM>
 __global__ void __launch_bounds__(kRcThreads, 1)
     bwd_recur_kernel(const __grid_constant__ CUtensorMap tmDZ, const __grid_constant__ CUtensorMap tmDA,
                      const __grid_constant__ CUtensorMap tmDY, const __grid_constant__ CUtensorMap tmWh,
@@ -763,13 +766,14 @@ __global__ void __launch_bounds__(kRcThreads, 1)
       };
       auto issue_w = [&](int s, const RcBlk& b) {
         uint8_t* dst = L.sB + s * kRcTile;
-        const int u0 = 256 * n1 + 128 * r;  // this CTA's 128 output units (MN-major boxes of 64)
+        const int u0 = 256 * n1 + 128 * r;  // this CTA's 128 output units
+        const CUtensorMap* tm = b.kind == 0 ? &tmWh : (b.kind == 1 ? &tmWdec : &tmWmh);
+        const uint64_t pw = b.kind == 0 ? pw2 : (b.kind == 1 ? pws : pw1);
+        if constexpr (WKM) {
+          ptx::tma_load_3d_2sm(dst, tm, bar0 + 8 * s, 64 * b.j, u0, 0, pw);
+        } else {  // MN-major boxes of 64 units
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          if (b.kind == 0) ptx::tma_load_3d_2sm(dst + i * 8192, &tmWh, bar0 + 8 * s, u0 + 64 * i, 64 * b.j, 0, pw2);
-          else if (b.kind == 1)
-            ptx::tma_load_3d_2sm(dst + i * 8192, &tmWdec, bar0 + 8 * s, u0 + 64 * i, 64 * b.j, 0, pws);
-          else ptx::tma_load_3d_2sm(dst + i * 8192, &tmWmh, bar0 + 8 * s, u0 + 64 * i, 64 * b.j, 0, pw1);
+          for (int i = 0; i < 2; ++i) ptx::tma_load_3d_2sm(dst + i * 8192, tm, bar0 + 8 * s, u0 + 64 * i, 64 * b.j, 0, pw);
         }
       };
       auto issue_a = [&](int s, const RcBlk& b) {
@@ -780,11 +784,13 @@ __global__ void __launch_bounds__(kRcThreads, 1)
       };
       auto prefetch_w = [&](const RcBlk& b) {
         const int u0 = 256 * n1 + 128 * r;
+        const CUtensorMap* tm = b.kind == 0 ? &tmWh : (b.kind == 1 ? &tmWdec : &tmWmh);
+        const uint64_t pw = b.kind == 0 ? pw2 : (b.kind == 1 ? pws : pw1);
+        if constexpr (WKM) {
+          ptx::tma_prefetch_3d(tm, 64 * b.j, u0, 0, pw);
+        } else {
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          if (b.kind == 0) ptx::tma_prefetch_3d(&tmWh, u0 + 64 * i, 64 * b.j, 0, pw2);
-          else if (b.kind == 1) ptx::tma_prefetch_3d(&tmWdec, u0 + 64 * i, 64 * b.j, 0, pws);
-          else ptx::tma_prefetch_3d(&tmWmh, u0 + 64 * i, 64 * b.j, 0, pw1);
+          for (int i = 0; i < 2; ++i) ptx::tma_prefetch_3d(tm, u0 + 64 * i, 64 * b.j, 0, pw);
         }
       };
       if (warp == 0) {
@@ -796,7 +802,7 @@ __global__ void __launch_bounds__(kRcThreads, 1)
   } else if (warp == 1) {
     if (leader && lane == 0) {  // ------------------------------------------------- MMA issuer
       uint32_t it = 0;
-      rc_consume<true>(L, it++, tmem + 256, false, tr);  // B2(T): dY_{T-1} W_dec
+      rc_consume<!WKM>(L, it++, tmem + 256, false, tr);  // B2(T): dY_{T-1} W_dec
       ptx::mma_commit_2sm_mc(&L.accf[1], 0x3);
 #pragma unroll 1
       for (int u = 0; u < T; ++u) {
@@ -808,7 +814,7 @@ __global__ void __launch_bounds__(kRcThreads, 1)
         tr.step(u, 2);
 #pragma unroll 1
         for (int i = 0; i < nB1; ++i) {
-          rc_consume<true>(L, it++, tmem, i > 0, tr);
+          rc_consume<!WKM>(L, it++, tmem, i > 0, tr);
           if (i == 0) tr.step(u, 3);
         }
         ptx::mma_commit_2sm_mc(&L.accf[0], 0x3);
@@ -818,7 +824,7 @@ __global__ void __launch_bounds__(kRcThreads, 1)
         ptx::tc_fence_after();
 #pragma unroll 1
         for (int i = 0; i < 1 + nB2; ++i) {
-          rc_consume<true>(L, it++, tmem + 256, i > 0, tr);
+          rc_consume<!WKM>(L, it++, tmem + 256, i > 0, tr);
           if (i == 1) tr.step(u, 5);
         }
         ptx::mma_commit_2sm_mc(&L.accf[1], 0x3);
