@@ -76,8 +76,9 @@ def kernel_table(h, e, B, T, persistent):
     return {
         "gemm_tc1s_kernel<4,EpiF1IO>": ("fwd_rec", T, 2.0 * B * h * h),            # a_t = H_{t-1} W_mh^T
         "gemm_tc2_kernel<256,EpiF2IO>": ("fwd_rec", T, 2.0 * B * 4 * h * h),       # z_t = M_t W_h^T (+ one-hot seg)
-        "gemm_tc1s_kernel<4,EpiB1IO>": ("bwd_rec", T, 2.0 * B * 4 * h * h),        # dM_t = dZ_t W_h
-        "gemm_tc1s_kernel<4,EpiB2>": ("bwd_rec", T - 1, 2.0 * B * (h + 256) * h),  # dA_t W_mh + dY_{t-1} W_dec
+        # the backward reads the weights MN-major (",BMN"): dM_t = dZ_t W_h; dA_t W_mh + dY_{t-1} W_dec
+        "gemm_tc1s_kernel<4,EpiB1IO,BMN>": ("bwd_rec", T, 2.0 * B * 4 * h * h),
+        "gemm_tc1s_kernel<4,EpiB2,BMN>": ("bwd_rec", T - 1, 2.0 * B * (h + 256) * h),
         "gemm_tc2_kernel<512,EpiWgrad,MN>": ("wgrad", 3, 2.0 * B * T * (5 * h * h + 256 * h) / 3),
         "gemm_tc2p_kernel<256,EpiY>": ("decoder", 1, 2.0 * B * T * 256 * h),
     }

@@ -159,9 +159,13 @@ struct Seg2 {
   int az2, bz2;
 };
 
-// MN: both operands MN-major ([K][M] / [K][N] in memory, the weight-gradient GEMMs D = A^T B over
-// a long K = T*B): each stage is one 64-row K block loaded as 64-wide MN boxes.
-template <class C, bool PAIR, bool MN = false>
+// MN (operand majors): 0 = both K-major; 1 = both MN-major ([K][M] / [K][N] in memory, the
+// weight-gradient GEMMs D = A^T B over a long K = T*B): each stage is one 64-row K block loaded as
+// 64-wide MN boxes; 2 = K-major A, MN-major B (the backward recurrence reading the row-major weight
+// working copies directly, no transposed copies).
+__host__ __device__ constexpr bool a_mn(int mn) { return mn == 1; }
+__host__ __device__ constexpr bool b_mn(int mn) { return mn != 0; }
+template <class C, bool PAIR, int MN = 0>
 __device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUtensorMap* tmA, const CUtensorMap* tmB,
                                              const CUtensorMap* tmA2, const CUtensorMap* tmB2, Seg2 sg, int nkb,
                                              int kb0, int m0, int nb0, int az, int bz, uint32_t polA,
@@ -173,7 +177,7 @@ __device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUten
   const uint64_t pa = ptx::make_policy(polA), pb = ptx::make_policy(polB);
   const uint32_t tx = PAIR ? 2 * C::STAGE_BYTES : C::STAGE_BYTES;
   auto loadA = [&](int s, int kb) {
-    if constexpr (MN) {
+    if constexpr (a_mn(MN)) {
 #pragma unroll
       for (int i = 0; i < C::BM / 64; ++i) {
         uint8_t* dst = L.sA + s * C::A_BYTES + i * 8192;
@@ -189,14 +193,17 @@ __device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUten
     else ptx::tma_load_3d(L.sA + s * C::A_BYTES, m, &L.full[s], k, m0, z, pa);
   };
   auto loadB = [&](int s, int kb) {
-    if constexpr (MN) {
-      static_assert(!MN || C::B_BYTES % 8192 == 0, "MN-major B needs 64-wide boxes per CTA");
+    if constexpr (b_mn(MN)) {
+      static_assert(C::B_BYTES % 8192 == 0, "MN-major B needs 64-wide boxes per CTA");
+      const bool s2 = kb >= sg.kb_seg0;  // second K segment (MN == 2 only; never for MN == 1)
+      const CUtensorMap* m = s2 ? tmB2 : tmB;
+      const int k = (s2 ? kb - sg.kb_seg0 : kb) * C::BK, z = s2 ? sg.bz2 : bz;
 #pragma unroll
       for (int i = 0; i < C::B_BYTES / 8192; ++i) {
         uint8_t* dst = L.sB + s * C::B_BYTES + i * 8192;
         const int col = C::BNT == 512 ? nb0 + (i >> 1) * 256 + (i & 1) * 64 : nb0 + 64 * i;
-        if (PAIR) ptx::tma_load_3d_2sm(dst, tmB, bar_leader0 + s * 8, col, kb * C::BK, bz, pb);
-        else ptx::tma_load_3d(dst, tmB, &L.full[s], col, kb * C::BK, bz, pb);
+        if (PAIR) ptx::tma_load_3d_2sm(dst, m, bar_leader0 + s * 8, col, k, z, pb);
+        else ptx::tma_load_3d(dst, m, &L.full[s], col, k, z, pb);
       }
       return;
     }
@@ -238,12 +245,13 @@ __device__ __forceinline__ void gemm_produce(const SmemLayout<C>& L, const CUten
 
 // MMA issuer (one thread of the leader CTA): BK/16 tcgen05.mma per stage, commit frees the stage;
 // the final commit signals the accumulator.  PAIR: M = 256 over the CTA pair, commits multicast.
-template <class C, bool PAIR, int MMA_N, bool MN = false>
+template <class C, bool PAIR, int MMA_N, int MN = 0>
 __device__ __forceinline__ void gemm_mma(const SmemLayout<C>& L, uint32_t tmem, int nkb, uint16_t pair_mask,
                                          uint64_t* trace_slot) {
   constexpr int MN_ = MMA_N > 256 ? 256 : MMA_N;  // BN = 512: two N = 256 MMAs per k-step
-  constexpr uint32_t idesc = ptx::idesc_f16_f32(PAIR ? 256 : 128, MN_, MN);
-  constexpr int kstep = MN ? 2048 >> 4 : 32 >> 4;  // descriptor start-address step per K = 16
+  constexpr uint32_t idesc = ptx::idesc_f16_f32_ab(PAIR ? 256 : 128, MN_, a_mn(MN), b_mn(MN));
+  // descriptor start-address step per K = 16: one 128-byte swizzle row group (MN-major) or 32 bytes
+  constexpr int akstep = a_mn(MN) ? 2048 >> 4 : 32 >> 4, bkstep = b_mn(MN) ? 2048 >> 4 : 32 >> 4;
 #pragma unroll 1
   for (int i = 0; i < nkb; ++i) {
     const int s = i % C::STAGES;
@@ -252,16 +260,16 @@ __device__ __forceinline__ void gemm_mma(const SmemLayout<C>& L, uint32_t tmem, 
     ptx::tc_fence_after();
     if (trace_slot && i == 0) *trace_slot = ptx::globaltimer();
     const uint32_t sa = ptx::smem_u32(L.sA + s * C::A_BYTES), sb = ptx::smem_u32(L.sB + s * C::B_BYTES);
-    const uint64_t ad = MN ? ptx::sdesc_mnmajor_sw128(sa) : ptx::sdesc_kmajor_sw128(sa);
-    const uint64_t bd = MN ? ptx::sdesc_mnmajor_sw128(sb) : ptx::sdesc_kmajor_sw128(sb);
+    const uint64_t ad = a_mn(MN) ? ptx::sdesc_mnmajor_sw128(sa) : ptx::sdesc_kmajor_sw128(sa);
+    const uint64_t bd = b_mn(MN) ? ptx::sdesc_mnmajor_sw128(sb) : ptx::sdesc_kmajor_sw128(sb);
 #pragma unroll
     for (int k = 0; k < C::BK / 16; ++k) {
-      if (PAIR) ptx::mma_f16_2sm(tmem, ad + kstep * k, bd + kstep * k, idesc, (i | k) != 0 ? 1u : 0u);
-      else ptx::mma_f16(tmem, ad + kstep * k, bd + kstep * k, idesc, (i | k) != 0 ? 1u : 0u);
+      if (PAIR) ptx::mma_f16_2sm(tmem, ad + akstep * k, bd + bkstep * k, idesc, (i | k) != 0 ? 1u : 0u);
+      else ptx::mma_f16(tmem, ad + akstep * k, bd + bkstep * k, idesc, (i | k) != 0 ? 1u : 0u);
       if constexpr (MMA_N == 512) {  // second half: B block at +16 KB, accumulator columns +256
         const uint64_t bd2 = bd + (16384 >> 4);
-        if (PAIR) ptx::mma_f16_2sm(tmem + 256, ad + kstep * k, bd2 + kstep * k, idesc, (i | k) != 0 ? 1u : 0u);
-        else ptx::mma_f16(tmem + 256, ad + kstep * k, bd2 + kstep * k, idesc, (i | k) != 0 ? 1u : 0u);
+        if (PAIR) ptx::mma_f16_2sm(tmem + 256, ad + akstep * k, bd2 + bkstep * k, idesc, (i | k) != 0 ? 1u : 0u);
+        else ptx::mma_f16(tmem + 256, ad + akstep * k, bd2 + bkstep * k, idesc, (i | k) != 0 ? 1u : 0u);
       }
     }
     if (PAIR) ptx::mma_commit_2sm_mc(&L.empty[s], pair_mask);
@@ -369,7 +377,7 @@ __device__ __forceinline__ void epi_begin(uint64_t* accf, bool have, uint64_t* t
   }
 
 // ---------------------------------------------------------------------------------------------
-template <int BN, class Epi, bool MN = false>
+template <int BN, class Epi, int MN = 0>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, Seg2 sg, int M,
@@ -447,7 +455,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 // ---------------------------------------------------------------------------------------------
-template <int BN, class Epi, bool MN = false>
+template <int BN, class Epi, int MN = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, Seg2 sg, int M,
@@ -541,7 +549,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 // i+1; the stage ring and its phases run on across tiles.  Barriers (leader CTA unless noted):
 // acc_full[b] (MMA commit, multicast to both CTAs) and acc_empty[b] (one arrive per epilogue warp
 // of both CTAs, the peer's remotely).  Epilogues run in their row form (run<NG>).
-template <int BN, class Epi, bool MN = false>
+template <int BN, class Epi, int MN = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_tc2p_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, Seg2 sg,
@@ -605,18 +613,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (leader) ptx::mbar_arrive_expect_tx(&L.full[s], tx);
           uint8_t* da = L.sA + s * C::A_BYTES;
           uint8_t* db = L.sB + s * C::B_BYTES;
-          if constexpr (MN) {
+          const bool s2 = kb >= sg.kb_seg0;  // second K segment (never with MN == 1)
+          const int k = (s2 ? kb - sg.kb_seg0 : kb) * C::BK;
+          if constexpr (a_mn(MN)) {
 #pragma unroll
             for (int i = 0; i < C::BM / 64; ++i)
               ptx::tma_load_3d_2sm(da + i * 8192, &tmA, bar0 + s * 8, m0 + 64 * i, kb * C::BK, az, pa);
-            static_assert(!MN || C::B_BYTES % 8192 == 0, "MN-major B needs 64-wide boxes per CTA");
+          } else {
+            ptx::tma_load_3d_2sm(da, s2 ? &tmA2 : &tmA, bar0 + s * 8, k, m0, s2 ? sg.az2 : az, pa);
+          }
+          if constexpr (b_mn(MN)) {
+            static_assert(C::B_BYTES % 8192 == 0, "MN-major B needs 64-wide boxes per CTA");
 #pragma unroll
             for (int i = 0; i < C::B_BYTES / 8192; ++i)
-              ptx::tma_load_3d_2sm(db + i * 8192, &tmB, bar0 + s * 8, nb0 + 64 * i, kb * C::BK, bz, pb);
+              ptx::tma_load_3d_2sm(db + i * 8192, s2 ? &tmB2 : &tmB, bar0 + s * 8, nb0 + 64 * i, k, s2 ? sg.bz2 : bz,
+                                   pb);
           } else {
-            const bool s2 = kb >= sg.kb_seg0;
-            const int k = (s2 ? kb - sg.kb_seg0 : kb) * C::BK;
-            ptx::tma_load_3d_2sm(da, s2 ? &tmA2 : &tmA, bar0 + s * 8, k, m0, s2 ? sg.az2 : az, pa);
             ptx::tma_load_3d_2sm(db, s2 ? &tmB2 : &tmB, bar0 + s * 8, k, nb0, s2 ? sg.bz2 : bz, pb);
           }
         }
@@ -625,8 +637,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_f16_f32(256, BN, MN);
-      constexpr int kstep = MN ? 2048 >> 4 : 32 >> 4;
+      constexpr uint32_t idesc = ptx::idesc_f16_f32_ab(256, BN, a_mn(MN), b_mn(MN));
+      constexpr int akstep = a_mn(MN) ? 2048 >> 4 : 32 >> 4, bkstep = b_mn(MN) ? 2048 >> 4 : 32 >> 4;
       int it = 0, lt = 0;
 #pragma unroll 1
       for (int tile = pid; tile < ntiles; tile += npairs, ++lt) {
@@ -641,11 +653,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           ptx::tc_fence_after();
           if (tracing && it == 0) tr_ts[2] = ptx::globaltimer();
           const uint32_t sa = ptx::smem_u32(L.sA + s * C::A_BYTES), sb = ptx::smem_u32(L.sB + s * C::B_BYTES);
-          const uint64_t ad = MN ? ptx::sdesc_mnmajor_sw128(sa) : ptx::sdesc_kmajor_sw128(sa);
-          const uint64_t bd = MN ? ptx::sdesc_mnmajor_sw128(sb) : ptx::sdesc_kmajor_sw128(sb);
+          const uint64_t ad = a_mn(MN) ? ptx::sdesc_mnmajor_sw128(sa) : ptx::sdesc_kmajor_sw128(sa);
+          const uint64_t bd = b_mn(MN) ? ptx::sdesc_mnmajor_sw128(sb) : ptx::sdesc_kmajor_sw128(sb);
 #pragma unroll
           for (int k = 0; k < C::BK / 16; ++k)
-            ptx::mma_f16_2sm(td, ad + kstep * k, bd + kstep * k, idesc, (kb | k) != 0 ? 1u : 0u);
+            ptx::mma_f16_2sm(td, ad + akstep * k, bd + bkstep * k, idesc, (kb | k) != 0 ? 1u : 0u);
           ptx::mma_commit_2sm_mc(&L.empty[s], 0x3);
         }
         ptx::mma_commit_2sm_mc(&acc_full[b], 0x3);
@@ -698,7 +710,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 // columns [z*256/S, (z+1)*256/S) of its 128 rows over the S partials in fixed order z' = 0..S-1
 // (deterministic) and runs the fused epilogue on that slice -- the 256 epilogue threads each take
 // half a row of the slice, or a whole row when the epilogue needs full 64-column chunks.
-template <int S, class Epi, bool MN = false>
+template <int S, class Epi, int MN = 0>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc1s_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, Seg2 sg, int M,

@@ -41,6 +41,12 @@ template <> struct EpiTag<EpiPartial> { static constexpr int value = 9; };
 template <class E> constexpr bool kMNEpi = false;
 template <typename S> constexpr bool kMNEpi<EpiWgrad<S>> = true;
 template <> constexpr bool kMNEpi<EpiPartial> = true;
+// epilogues of the backward recurrence's GEMMs, whose B operand (a weight) may be read MN-major
+// straight from its row-major working copy (K-major A, MN-major B)
+template <class E> constexpr bool kBMNEpi = false;
+template <typename S> constexpr bool kBMNEpi<EpiB1IO<S>> = true;
+template <typename S> constexpr bool kBMNEpi<EpiB1<S>> = true;
+template <typename S> constexpr bool kBMNEpi<EpiB2<S>> = true;
 }  // namespace mlstm
 
 namespace {
@@ -127,6 +133,7 @@ struct mlstm_ctx {
   // persistent dataflow recurrence (recur.cuh): mlstm_config.recurrence = 1 (or MLSTM_RECUR=1)
   int recur_env = 1;
   int recur_ok = -1;
+  bool bwd_needs_transposes = true;  // decided while recording graph A (enqueue_train_a)
   int rc_wkm = 0;                 // MLSTM_RC_WKM=1: persistent BPTT reads the transposed (K-major) weights
   int rc_exp = 0;                 // MLSTM_RC_EXP: timing experiments (wrong results), see RcPolicy
   int rc_rotate = 1;              // MLSTM_RC_ROTATE
@@ -476,7 +483,7 @@ cudaError_t launch_gemm(mlstm_ctx* c, Kern kern, dim3 grid, int smem, int cluste
   return e;
 }
 
-template <int BN, class Epi, bool MN = false>
+template <int BN, class Epi, int MN = 0>
 cudaError_t launch_tc(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, const CUtensorMap* ma2,
                       const CUtensorMap* mb2, Seg2 sg, int M, int N, int K, int az, int bz,
                       uint32_t pa, uint32_t pb, int flags, int splits, PrefetchJob pj,
@@ -486,7 +493,7 @@ cudaError_t launch_tc(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb
                      1, *ma, *mb, *ma2, *mb2, sg, M, N, K, az, bz, kbps, pa, pb, flags, pj, epi);
 }
 
-template <int S, class Epi, bool MN = false>
+template <int S, class Epi, int MN = 0>
 cudaError_t launch_tc1s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, const CUtensorMap* ma2,
                         const CUtensorMap* mb2, Seg2 sg, int M, int N, int K, int az,
                         int bz, uint32_t pa, uint32_t pb, int flags, PrefetchJob pj,
@@ -498,7 +505,7 @@ cudaError_t launch_tc1s(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* 
                      S, *ma, *mb, *ma2, *mb2, sg, M, N, K, az, bz, kbps, pa, pb, flags, pj, c->split_scratch, epi);
 }
 
-template <int BN, class Epi, bool MN = false>
+template <int BN, class Epi, int MN = 0>
 cudaError_t launch_tc2(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, const CUtensorMap* ma2,
                        const CUtensorMap* mb2, Seg2 sg, int M, int N, int K, int az,
                        int bz, uint32_t pa, uint32_t pb, int flags, int splits, PrefetchJob pj,
@@ -508,7 +515,7 @@ cudaError_t launch_tc2(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* m
                      Tc2Cfg<BN>::SMEM, 2, *ma, *mb, *ma2, *mb2, sg, M, N, K, az, bz, kbps, pa, pb, flags, pj, epi);
 }
 
-template <int BN, class Epi, bool MN = false>
+template <int BN, class Epi, int MN = 0>
 cudaError_t launch_tc2p(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* mb, const CUtensorMap* ma2,
                         const CUtensorMap* mb2, Seg2 sg, int M, int N, int K, int az, int bz, uint32_t pa,
                         uint32_t pb, int flags, PrefetchJob pj, const Epi& epi) {
@@ -518,8 +525,9 @@ cudaError_t launch_tc2p(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* 
                      *mb2, sg, M, N, K, az, bz, 0, pa, pb, flags, pj, epi);
 }
 
-// Engine dispatch for one plan (MN: both operands MN-major).
-template <bool MN, class Epi>
+// Engine dispatch for one plan (MN: 0 both operands K-major, 1 both MN-major, 2 K-major A with
+// MN-major B; MN-major B needs at least 64 B rows per CTA, so pair tiles of BN = 64 are refused).
+template <int MN, class Epi>
 cudaError_t dispatch_tc(mlstm_ctx* c, const Plan& p, const CUtensorMap* ma, const CUtensorMap* mb,
                         const CUtensorMap* ma2, const CUtensorMap* mb2, Seg2 sg, int M, int N, int K, int az, int bz,
                         uint32_t pa, uint32_t pb, int gflags, PrefetchJob pj, const Epi& epi) {
@@ -533,12 +541,14 @@ cudaError_t dispatch_tc(mlstm_ctx* c, const Plan& p, const CUtensorMap* ma, cons
       return launch_tc2<512, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
   }
   if (p.pair) {
-    if (MN || p.bn == 256)
+    if (MN == 1 || p.bn == 256)
       return launch_tc2<256, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
-    if constexpr (!MN) {
+    if constexpr (MN != 1) {
       if (p.bn == 128)
-        return launch_tc2<128, Epi>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
-      return launch_tc2<64, Epi>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
+        return launch_tc2<128, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
+      if constexpr (MN == 0)
+        return launch_tc2<64, Epi>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
+      return cudaErrorInvalidValue;
     }
   }
   switch (p.bn) {
@@ -547,6 +557,9 @@ cudaError_t dispatch_tc(mlstm_ctx* c, const Plan& p, const CUtensorMap* ma, cons
     default: return launch_tc<64, Epi, MN>(c, ma, mb, ma2, mb2, sg, M, N, K, az, bz, pa, pb, gflags, p.splits, pj, epi);
   }
 }
+
+// Whether the plan p can read an MN-major B operand (dispatch_tc<2>).
+inline bool bmn_plan_ok(const Plan& p) { return !(p.pair && !p.cluster && !(p.persist && p.splits == 1) && p.bn < 128); }
 
 // D[M x N] = A[az] . B[bz]^T, fused epilogue.  `splits` > 1 only with a partial epilogue.
 // Optional L2 prefetch of the next GEMM's weight operand (see l2_prefetch in gemm.cuh).
@@ -593,17 +606,23 @@ mlstm_status gemm(mlstm_ctx* c, const Opd& A, int az, const Opd& B, int bz, int 
     }
     const Seg2 sg{seg.A2 ? (K + 63) / 64 : (1 << 30), seg.az2, 0};
     const int Kt = seg.A2 ? ((K + 63) / 64) * 64 + seg.K2 : K;  // the kernels' K runs over both segments
-    if (A.mn != B.mn || (A.mn && seg.A2)) return fail(MLSTM_EINVAL, "gemm: mixed operand majors / MN segment");
+    if ((A.mn && !B.mn) || (A.mn && seg.A2) || (seg.B2 && seg.B2->mn != B.mn))
+      return fail(MLSTM_EINVAL, "gemm: unsupported operand majors / MN segment");
     if constexpr (kMNEpi<Epi>) {
       if (A.mn) {
         if (p.pair && p.bn < 128) return fail(MLSTM_EINVAL, "gemm: MN-major pair tiles need BN >= 128");
-        e = dispatch_tc<true>(c, p, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi);
+        e = dispatch_tc<1>(c, p, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi);
       } else {
-        e = dispatch_tc<false>(c, p, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi);
+        e = dispatch_tc<0>(c, p, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi);
       }
+    } else if constexpr (kBMNEpi<Epi>) {
+      if (A.mn) return fail(MLSTM_EINVAL, "gemm: MN-major A only for weight-gradient epilogues");
+      if (B.mn && !bmn_plan_ok(p)) return fail(MLSTM_EINVAL, "gemm: MN-major B needs pair tiles of BN >= 128");
+      e = B.mn ? dispatch_tc<2>(c, p, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi)
+               : dispatch_tc<0>(c, p, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi);
     } else {
-      if (A.mn) return fail(MLSTM_EINVAL, "gemm: MN-major operands only for weight-gradient epilogues");
-      e = dispatch_tc<false>(c, p, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi);
+      if (A.mn || B.mn) return fail(MLSTM_EINVAL, "gemm: MN-major operands only for weight-gradient / BPTT epilogues");
+      e = dispatch_tc<0>(c, p, ma, mb, ma2, mb2, sg, M, N, Kt, az, bz, A.pol, B.pol, gflags, pj, epi);
     }
     CUDA_OR_FAIL(c, e);
     return MLSTM_OK;
@@ -767,7 +786,8 @@ mlstm_status enqueue_transposes(mlstm_ctx* c) {
   const int h = c->h;
   dim3 blk(32, 8);
   if constexpr (std::is_same<S, __half>::value) {  // h is a multiple of 64
-    if (recur_on(c) && !c->rc_wkm) return MLSTM_OK;  // the persistent backward reads W_h, W_mh, W_dec MN-major
+    // the backward reads W_h, W_mh, W_dec MN-major (persistent kernel, or per-timestep plans that allow it)
+    if (!c->bwd_needs_transposes && !(recur_on(c) && c->rc_wkm)) return MLSTM_OK;
     LAUNCH(c, (transpose64_kernel<<<dim3(h / 64, h / 64), blk, 0, c->stream>>>(n.Wmh_w, n.WmhT, h, h)));
     LAUNCH(c, (transpose64_kernel<<<dim3(h / 64, 4 * h / 64), blk, 0, c->stream>>>(n.Wh_w, n.WhT, 4 * h, h)));
     LAUNCH(c, (transpose64_kernel<<<dim3(h / 64, 256 / 64), blk, 0, c->stream>>>(n.Wdec_w, n.WdecT, 256, h)));
@@ -938,28 +958,36 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
   phase(c, PH_BWD);
   bool rc = false;
   if constexpr (std::is_same<S, __half>::value) rc = recur_on(c);
+  const Plan p1 = plan_gemm(c->tc, B, h, 4 * h, false), p2 = plan_gemm(c->tc, B, h, h, false);
+  const Plan p0 = plan_gemm(c->tc, B, h, 256, false);
+  const bool persist = !rc && std::is_same<S, __half>::value && bwd_persist_ok(c);
+  // the per-timestep backward reads W_h, W_mh, W_dec MN-major straight from the row-major working
+  // copies (no transposed copies) whenever its tile plans allow it (tensor-core path)
+  const bool bmn = c->tc && !rc && !persist && !n.dHdec && bmn_plan_ok(p0) && bmn_plan_ok(p1) && bmn_plan_ok(p2);
+  c->bwd_needs_transposes = !rc && !bmn;
+  const Opd WdecB = bmn ? Opd{n.Wdec_w, h, 256, h, 1, 256L * h, 0, true, true} : WdecT;
   if (rc) {
     RET_IF(launch_bwd_recur(c));
   } else if (n.dHdec) {
     LAUNCH(c, (gate_bwd_last_kernel<S><<<grid_for((long)B * h / 16), 256, 0, c->stream>>>(n)));
   } else {  // gate backward of the last timestep: dH = dY_{T-1} W_dec only (TBTT: no recurrent term)
-    RET_IF(gemm<S>(c, dYs, T - 1, WdecT, 0, B, h, 256, plan_gemm(c->tc, B, h, 256, false), EpiB2<S>{n, T - 1}));
+    RET_IF(gemm<S>(c, dYs, T - 1, WdecB, 0, B, h, 256, p0, EpiB2<S>{n, T - 1}));
   }
   Segment segd;  // B2's second K segment: + dY_{t-1} W_dec
   if (!n.dHdec && !rc) {
     segd.A2 = &dYs;
-    segd.B2 = &WdecT;
+    segd.B2 = &WdecB;
     segd.K2 = 256;
   }
   {
     const Opd dZ{n.G5 + h, B, 4L * h, 5L * h, T, 5L * B * h, kPolFirst};  // dZ_t = slot t, cols [h, 5h)
-    const Opd WhT{n.WhT, h, 4L * h, 4L * h, 1, 4L * h * h, pol_last(c->l2_wh), true};
+    const Opd WhT = bmn ? Opd{n.Wh_w, h, 4L * h, h, 1, 4L * h * h, pol_last(c->l2_wh), true, true}
+                        : Opd{n.WhT, h, 4L * h, 4L * h, 1, 4L * h * h, pol_last(c->l2_wh), true};
     const Opd dA{n.dA, B, h, h, T, (long)B * h, kPolFirst};
-    const Opd WmhT{n.WmhT, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh), true};
-    const Plan p1 = plan_gemm(c->tc, B, h, 4 * h, false), p2 = plan_gemm(c->tc, B, h, h, false);
+    const Opd WmhT = bmn ? Opd{n.Wmh_w, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh), true, true}
+                         : Opd{n.WmhT, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh), true};
     // B2 prefetches into L2 the first k-blocks (of each K split) of the W_h^T tiles B1 streams next
     const size_t es = sizeof(S);
-    const bool persist = !rc && std::is_same<S, __half>::value && bwd_persist_ok(c);
     if (persist) RET_IF(launch_bwd_persist(c));
     for (int t = (persist || rc) ? -1 : T - 1; t >= 0; --t) {
       // B1(t) prefetches what B2's gate backward of step t-1 reads (written long ago by the
@@ -973,7 +1001,7 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
         if (n.dHdec) pb1.add(n.dHdec + (long)(t - 1) * BH, BH * 4L);
         pb2.add(n.Astash + (long)(t - 1) * BH, BH * (long)es);
       }
-      if (c->pf_bwd > 0 && c->tc) pb2.add(n.WhT, (long)(c->pf_bwd * 8.0 * h * h));
+      if (c->pf_bwd > 0 && c->tc && !bmn) pb2.add(n.WhT, (long)(c->pf_bwd * 8.0 * h * h));
       if (c->tc && c->async_epi)
         RET_IF(gemm<S>(c, dZ, t, WhT, 0, B, h, 4 * h, p1, EpiB1IO<S>{{n, t}}, pb1));
       else

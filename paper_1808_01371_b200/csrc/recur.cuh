@@ -53,7 +53,7 @@ struct RcPolicy {  // L2 policy codes (ptx::make_policy) of the operand streams
                    // read the shared activation chunks in the same order (same lines requested together)
   int exp;         // timing experiments only (wrong results): bit 0 = F2 A from chunk 0, bit 1 = F2 B block 0,
                    // bit 2 = no F2 A loads, bit 3 = no F2 B loads, bit 4 = no readiness flags (races),
-                   // bit 5 = bare forward epilogue (no reduce / stores)
+                   // bit 5 = bare forward epilogue (no reduce / stores); bit 6 = no per-k-block trace records
 };
 
 // One operand k-block of the producer's stream: its readiness flag (null = no dependency, e.g. a
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(kRcThreads, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem = *L.tmem_slot;
-  const RcTrace tr{tr_base_s, T, kRcTraceStep * per, per, 3000};
+  const RcTrace tr{tr_base_s, T, kRcTraceStep * per, (pol.exp & 64) ? 0 : per, 3000};
 
   if (warp == 0 || warp == kRcActWarp) {
     {  // ----------------------------------------------------------- TMA producers (weights, activations)
@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(kRcThreads, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem = *L.tmem_slot;
-  const RcTrace tr{tr_base_s, T, 1 + kRcTraceStep * per, per, 4000};
+  const RcTrace tr{tr_base_s, T, 1 + kRcTraceStep * per, (pol.exp & 64) ? 0 : per, 4000};
   const int total = 1 + T * per - (1 + nB2);  // no B2(0)
 
   if (warp == 0 || warp == kRcActWarp) {

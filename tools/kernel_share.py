@@ -23,7 +23,7 @@ PHASE_OF = {  # kernel-name prefix -> bench phase
 def short(name):
     n = name.replace("void ", "").replace("mlstm::", "")
     n = n.split("(CUtensorMap")[0].split("(Net")[0].split("(const")[0]
-    return n.replace("<__half>", "").replace(", 0>", ">").replace(", 1>", ",MN>").replace(" ", "")
+    return n.replace("<__half>", "").replace(", 0>", ">").replace(", 1>", ",MN>").replace(", 2>", ",BMN>").replace(" ", "")
 
 
 def main():
