@@ -65,26 +65,30 @@ def phase_flops(h, e, B, T):
     }
 
 
-def kernel_table(h, e, B, T, persistent):
+def kernel_table(h, e, B, T, kind):
     """The kernels of each GEMM phase of one step: name -> (phase, launches per step, algorithmic FLOP per
-    launch).  Names match profiles/ncu_kernel_share.json (tools/kernel_share.py)."""
-    if persistent:
-        pf = phase_flops(h, e, B, T)
-        return {"fwd_recur_kernel": ("fwd_rec", 1, pf["fwd_rec"]), "bwd_recur_kernel": ("bwd_rec", 1, pf["bwd_rec"]),
-                "gemm_tc2_kernel<512,EpiWgrad,MN>": ("wgrad", 3, 2.0 * B * T * (5 * h * h + 256 * h) / 3),
-                "gemm_tc2p_kernel<256,EpiY>": ("decoder", 1, 2.0 * B * T * 256 * h)}
-    return {
-        "gemm_tc1s_kernel<4,EpiF1IO>": ("fwd_rec", T, 2.0 * B * h * h),            # a_t = H_{t-1} W_mh^T
-        "gemm_tc2_kernel<256,EpiF2IO>": ("fwd_rec", T, 2.0 * B * 4 * h * h),       # z_t = M_t W_h^T (+ one-hot seg)
-        # the backward reads the weights MN-major (",BMN"): dM_t = dZ_t W_h; dA_t W_mh + dY_{t-1} W_dec
-        "gemm_tc1s_kernel<4,EpiB1IO,BMN>": ("bwd_rec", T, 2.0 * B * 4 * h * h),
-        "gemm_tc1s_kernel<4,EpiB2,BMN>": ("bwd_rec", T - 1, 2.0 * B * (h + 256) * h),
+    launch).  Names match profiles/ncu_kernel_share.json (tools/kernel_share.py).  kind: the
+    recurrence implementation (mlstm_recurrence_kind: 0 per-timestep, 1 persistent, 3 persistent
+    forward + per-timestep BPTT)."""
+    pf = phase_flops(h, e, B, T)
+    tab = {
         "gemm_tc2_kernel<512,EpiWgrad,MN>": ("wgrad", 3, 2.0 * B * T * (5 * h * h + 256 * h) / 3),
         "gemm_tc2p_kernel<256,EpiY>": ("decoder", 1, 2.0 * B * T * 256 * h),
     }
+    if kind in (1, 3):
+        tab["fwd_recur_kernel"] = ("fwd_rec", 1, pf["fwd_rec"])
+    else:
+        tab["gemm_tc1s_kernel<4,EpiF1IO>"] = ("fwd_rec", T, 2.0 * B * h * h)        # a_t = H_{t-1} W_mh^T
+        tab["gemm_tc2_kernel<256,EpiF2IO>"] = ("fwd_rec", T, 2.0 * B * 4 * h * h)   # z_t = M_t W_h^T (+ one-hot seg)
+    if kind == 1:
+        tab["bwd_recur_kernel"] = ("bwd_rec", 1, pf["bwd_rec"])
+    else:  # the backward reads the weights MN-major (",BMN"): dM_t = dZ_t W_h; dA_t W_mh + dY_{t-1} W_dec
+        tab["gemm_tc1s_kernel<4,EpiB1IO,BMN>"] = ("bwd_rec", T, 2.0 * B * 4 * h * h)
+        tab["gemm_tc1s_kernel<4,EpiB2,BMN>"] = ("bwd_rec", T - 1, 2.0 * B * (h + 256) * h)
+    return tab
 
 
-def kernel_shares(persistent):
+def kernel_shares(kind):
     """phase -> {kernel: share of the phase's kernel time}."""
     out = {}
     try:
@@ -92,8 +96,10 @@ def kernel_shares(persistent):
         out = {ph: {k: v["share"] for k, v in ks.items()} for ph, ks in tab.items()}
     except (OSError, ValueError, KeyError):
         pass
-    if persistent:  # one kernel per recurrence phase
-        out.update({"fwd_rec": {"fwd_recur_kernel": 1.0}, "bwd_rec": {"bwd_recur_kernel": 1.0}})
+    if kind in (1, 3):  # one kernel per persistent recurrence phase
+        out["fwd_rec"] = {"fwd_recur_kernel": 1.0}
+    if kind == 1:
+        out["bwd_rec"] = {"bwd_recur_kernel": 1.0}
     return out
 
 
@@ -258,8 +264,9 @@ def main():
     ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
     ap.add_argument("--weight-norm", action="store_true",
                     help="weight-normalised LSTM matrices (P:150; SURVEY NEXT #1)")
-    ap.add_argument("--recurrence", type=int, default=0, choices=[0, 1, 2],
-                    help="mlstm_config.recurrence: 0 library default, 1 persistent dataflow kernels, 2 per-timestep")
+    ap.add_argument("--recurrence", type=int, default=0, choices=[0, 1, 2, 3],
+                    help="mlstm_config.recurrence: 0 library default, 1 persistent dataflow kernels, 2 per-timestep, "
+                         "3 persistent forward + per-timestep BPTT")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=15.0)
@@ -374,8 +381,8 @@ def main():
     gem = {k: phases[k] for k in pf if k in phases}
     # dominant kernel: phase time (live events) x the kernel's share of that phase (committed ncu
     # launch list, tools/kernel_share.py); per-launch time = that / its launches per step
-    persistent = model.uses_recur()
-    ktab, shares = kernel_table(h, e, B, T, persistent), kernel_shares(persistent)
+    kind = M.lib().mlstm_recurrence_kind(model.ctx)
+    ktab, shares = kernel_table(h, e, B, T, kind), kernel_shares(kind)
     kt = {}
     for k, (ph, nl, fl) in ktab.items():
         sh = shares.get(ph, {}).get(k)
@@ -415,7 +422,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_median": med, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f16 (fp32 accumulate, fp32 masters)", "data": "synthetic",
         "config": {"workload": desc, "global_batch": world * B, "seq_len": T, "parallelism": f"dp{world}",
-                   "recurrence": "persistent dataflow kernels" if persistent else "per-timestep GEMM launches",
+                   "recurrence": {1: "persistent dataflow kernels", 3: "persistent forward, per-timestep BPTT"}.get(
+                       kind, "per-timestep GEMM launches"),
                    "l2": "no flush: per-step working set (~11 GB) >> 126 MB L2"},
         "roofline": roof, "roofline_phases": roof_phases,
         "step_tflops_per_gpu": whole, "step_frac_of_sustained_peak": whole / sustained,

@@ -74,8 +74,9 @@ typedef struct {
                           faster implementation as measured), 1 = the persistent
                           dataflow kernels (one launch for the T forward timesteps and one for BPTT;
                           mixed precision, 256 rows per micro-batch, h a multiple of 256 <= 4736,
-                          otherwise the per-timestep path), 2 = per-timestep.  MLSTM_RECUR=0/1 in the
-                          environment at mlstm_init overrides (A/B measurements).             */
+                          otherwise the per-timestep path), 2 = per-timestep, 3 = persistent
+                          forward with per-timestep BPTT.  MLSTM_RECUR=0/1 in the environment at
+                          mlstm_init overrides (A/B measurements).                             */
 } mlstm_config;
 
 /* Result of one step; every field is the global value over all ranks. */
@@ -210,8 +211,9 @@ const char* mlstm_phase_name(int phase);
 int32_t mlstm_launches_per_step(mlstm_ctx* ctx);
 
 /* Which implementation runs the recurrence ("sequential nature"; north_star kernels (b), (c-1)):
- * 1 = the persistent dataflow kernels (mlstm_config.recurrence = 1 and a covered shape), 0 = one
- * tcgen05 / SIMT GEMM launch per timestep and GEMM.  -1 for a null context. */
+ * 1 = the persistent dataflow kernels (mlstm_config.recurrence = 1 and a covered shape), 3 = the
+ * persistent forward with per-timestep BPTT (recurrence = 3), 0 = one tcgen05 / SIMT GEMM launch per
+ * timestep and GEMM.  -1 for a null context. */
 int32_t mlstm_recurrence_kind(mlstm_ctx* ctx);
 
 /* Diagnostics: times `iters` launches of the tensor-core GEMM engine on random fp16 operands

@@ -133,6 +133,7 @@ struct mlstm_ctx {
   // persistent dataflow recurrence (recur.cuh): mlstm_config.recurrence = 1 (or MLSTM_RECUR=1)
   int recur_env = 1;
   int recur_ok = -1;
+  bool recur_fwd_only = false;  // recurrence = 3: persistent forward, per-timestep BPTT
   bool bwd_needs_transposes = true;  // decided while recording graph A (enqueue_train_a)
   int rc_wkm = 0;                 // MLSTM_RC_WKM=1: persistent BPTT reads the transposed (K-major) weights
   int rc_exp = 0;                 // MLSTM_RC_EXP: timing experiments (wrong results), see RcPolicy
@@ -346,7 +347,7 @@ mlstm_status validate(const mlstm_config* cfg) {
     return fail(MLSTM_EINVAL, "micro_batch must be 0 (= batch) or divide batch");
   if (cfg->weight_norm != 0 && cfg->weight_norm != 1) return fail(MLSTM_EINVAL, "weight_norm must be 0 or 1 (Q24)");
   if (cfg->precision != MLSTM_FP32 && cfg->precision != MLSTM_MIXED) return fail(MLSTM_EINVAL, "bad precision");
-  if (cfg->recurrence < 0 || cfg->recurrence > 2) return fail(MLSTM_EINVAL, "recurrence must be 0, 1 or 2");
+  if (cfg->recurrence < 0 || cfg->recurrence > 3) return fail(MLSTM_EINVAL, "recurrence must be 0, 1, 2 or 3");
   if (!(cfg->decay_iters > 0) || !(cfg->lr0 >= 0)) return fail(MLSTM_EINVAL, "bad LR schedule");
   if (!(cfg->scale_min > 0) || !(cfg->scale_max >= cfg->scale_min) || !(cfg->scale_init >= cfg->scale_min) ||
       !(cfg->scale_init <= cfg->scale_max) || cfg->scale_growth_interval <= 0)
@@ -356,7 +357,9 @@ mlstm_status validate(const mlstm_config* cfg) {
 
 void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   c->cfg = *cfg;
-  c->recur_env = cfg->recurrence == 1 ? 1 : 0;  // 0 (default) and 2: per-timestep launches
+  // 1: persistent forward + BPTT; 3: persistent forward, per-timestep BPTT; 0 (default), 2: per-timestep
+  c->recur_env = (cfg->recurrence == 1 || cfg->recurrence == 3) ? 1 : 0;
+  c->recur_fwd_only = cfg->recurrence == 3;
   c->h = cfg->hidden;
   c->e = cfg->embed;
   c->Bfull = cfg->batch;
@@ -957,7 +960,7 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
   }
   phase(c, PH_BWD);
   bool rc = false;
-  if constexpr (std::is_same<S, __half>::value) rc = recur_on(c);
+  if constexpr (std::is_same<S, __half>::value) rc = recur_on(c) && !c->recur_fwd_only;
   const Plan p1 = plan_gemm(c->tc, B, h, 4 * h, false), p2 = plan_gemm(c->tc, B, h, h, false);
   const Plan p0 = plan_gemm(c->tc, B, h, 256, false);
   const bool persist = !rc && std::is_same<S, __half>::value && bwd_persist_ok(c);
@@ -1786,7 +1789,7 @@ int32_t mlstm_launches_per_step(mlstm_ctx* c) {
 
 int32_t mlstm_recurrence_kind(mlstm_ctx* c) {
   if (!c) return -1;
-  return recur_on(c) ? 1 : 0;
+  return recur_on(c) ? (c->recur_fwd_only ? 3 : 1) : 0;
 }
 
 mlstm_status mlstm_gemm_bench(int engine, int M, int N, int K, int bn, int iters, double* ms) {

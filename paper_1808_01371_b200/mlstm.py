@@ -383,7 +383,7 @@ class MLSTM:
 
     def uses_recur(self) -> bool:
         """True when the recurrence runs on the persistent dataflow kernels (mlstm_recurrence_kind)."""
-        return lib().mlstm_recurrence_kind(self.ctx) == 1
+        return lib().mlstm_recurrence_kind(self.ctx) in (1, 3)
 
     def launches_per_step(self) -> int:
         n = lib().mlstm_launches_per_step(self.ctx)

@@ -20,12 +20,13 @@ from gpu_helpers import TOL, compare_grads, inputs, make_model, oracle_step, ora
 
 
 def _model(h, T, recur, **kw):
-    return make_model(h, 64, 256, T, "mixed", recurrence=1 if recur else 2, **kw)
+    return make_model(h, 64, 256, T, "mixed", recurrence=kw.pop("recurrence", 1 if recur else 2), **kw)
 
 
-@pytest.mark.parametrize("h,T", [(256, 1), (256, 6), (1024, 5)])
-def test_recur_step_matches_oracle(h, T):
-    m = _model(h, T, True)
+@pytest.mark.parametrize("h,T,recurrence", [(256, 1, 1), (256, 6, 1), (1024, 5, 1), (256, 6, 3), (1024, 5, 3)])
+def test_recur_step_matches_oracle(h, T, recurrence):
+    """recurrence 1: persistent forward and BPTT; 3: persistent forward, per-timestep BPTT."""
+    m = _model(h, T, True, recurrence=recurrence)
     assert m.uses_recur(), "the persistent recurrence did not engage for this shape"
     theta0 = oracle_theta(h, 64)
     by = inputs(256, T)
