@@ -79,6 +79,9 @@ struct TcCfg {  // one CTA per 128 x BN tile
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512;
   static_assert(STAGES * STAGE_BYTES >= kEpiWarps * kWarpStageBytes, "epilogue staging windows");
 };
+#ifndef MLSTM_TC2_STAGES256
+#define MLSTM_TC2_STAGES256 6  // ring depth of the 256 x 256 CTA-pair tiles (A/B builds override)
+#endif
 template <int BN>
 struct Tc2Cfg {  // CTA pair per 256 x BN tile: per CTA 128 rows of A, BN/2 rows of B
   // BN = 512: two N = 256 MMAs per k-step into TMEM columns [0,256) and [256,512); each CTA holds
@@ -87,7 +90,7 @@ struct Tc2Cfg {  // CTA pair per 256 x BN tile: per CTA 128 rows of A, BN/2 rows
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 512 ? 4 : BN == 256 ? 6 : (BN == 128 ? 8 : 10);
+  static constexpr int STAGES = BN == 512 ? 4 : BN == 256 ? MLSTM_TC2_STAGES256 : (BN == 128 ? 8 : 10);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512;
   static_assert(STAGES * STAGE_BYTES >= kEpiWarps * kWarpStageBytes, "epilogue staging windows");
 };
