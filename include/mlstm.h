@@ -103,9 +103,10 @@ size_t mlstm_workspace_bytes(const mlstm_config* cfg);
 /* The gradient allreduce's bucket plan for `world` ranks (fp16 SUM of the weight gradients;
  * SURVEY 8(e)), host only: element ranges of the canonical gradient layout, in the order they are
  * reduced.  out: host int64 [cap][3] = (offset, count, after) per bucket, after = the work the bucket
- * waits for: 0 = the first row half of dW_h (units [0, h/2) of every gate; four contiguous ranges),
- * 1 = dW_h, 2 = dW_mh, 3 = every other gradient (end of the backward).  The buckets tile [0, P) exactly
- * once.  world == 1, micro-batching or MLSTM_AR_OVERLAP=0: one bucket [0, P) after 3.  *n = number of
+ * waits for: 0 = dW_dec (computed before BPTT; the bucket is W_dec and b_dec and overlaps the backward),
+ * 1 = the first row half of dW_h (units [0, h/2) of every gate; four contiguous ranges), 2 = dW_h,
+ * 3 = dW_mh, 4 = every other gradient (end of the backward).  The buckets tile [0, P) exactly once.
+ * world == 1, micro-batching or MLSTM_AR_OVERLAP=0: one bucket [0, P) after 4.  *n = number of
  * buckets; MLSTM_EINVAL if cap < *n (then *n is still set) or the config is invalid. */
 mlstm_status mlstm_allreduce_plan(const mlstm_config* cfg, int32_t world, int64_t* out, int32_t cap, int32_t* n);
 

@@ -124,7 +124,8 @@ struct mlstm_ctx {
   // the weight-gradient GEMM producing them finishes (W_h, then W_mh, then the rest), overlapping
   // the remaining weight-gradient work; MLSTM_AR_OVERLAP=0 reduces after graph A.
   cudaStream_t comm_stream = nullptr;
-  cudaEvent_t ev_wh = nullptr, ev_wmh = nullptr, ev_a_end = nullptr, ev_comm = nullptr, ev_wh_a = nullptr;
+  cudaEvent_t ev_wh = nullptr, ev_wmh = nullptr, ev_a_end = nullptr, ev_comm = nullptr, ev_wh_a = nullptr,
+              ev_wdec = nullptr;
   bool ar_overlap = true;
   int force_plan = 0;          // MLSTM_FORCE_PLAN (test instrument), applied while this ctx enqueues
   bool wgrad512 = true;        // weight gradients on 256 x 512 pair tiles (MLSTM_WGRAD512=0: 256 x 256)
@@ -958,6 +959,52 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
     Opd A{n.dY, (long)T * B, 256, 256, 1, (long)T * B * 256};
     RET_IF(gemm<S>(c, A, 0, WdecT, 0, T * B, h, 256, plan_gemm(c->tc, (long)T * B, h, 256, false), EpiDHdec<S>{n}));
   }
+  // dW_dec = dY^T H needs only the forward and the CE: it runs before BPTT, and with several ranks its
+  // allreduce bucket (W_dec, b_dec: SURVEY 8(e) "bucket 0") overlaps the backward
+  struct W {
+    Opd A, B;
+    long M, N, off;
+    int mode;
+  };
+  // every operand MN-major: the row-major [T*B][cols] stashes the recurrence wrote, K = (t, b)
+  auto mn = [&](const void* p, long cols, long ld) { return Opd{p, cols, Kt, ld, 1, 0, 0, false, true}; };
+  const W ws[4] = {
+      {mn(n.G5 + h, 4L * h, 5L * h), mn(n.Mrm, h, h), 4L * h, h, c->po.Wh, 1},      // dW_h = dZ^T M
+      {mn(n.dA, h, h), mn(n.Hrm, h, h), h, h, c->po.Wmh, 0},                         // dW_mh = dA^T H_{t-1}
+      {mn(n.dY, 256, 256), mn(n.Hrm + (long)B * h, h, h), 256, h, c->po.Wdec, 0},    // dW_dec = dY^T H
+      {mn(n.OHR, 256, 256), mn(n.G5, 5L * h, 5L * h), 256, 5L * h, 0, 2},          // S = onehot^T [dMX|dZ]
+  };
+  // one weight-gradient job (plan, optional dW_h row halves, split-K finaliser, bucket event)
+  auto run_w = [&](int wi) -> mlstm_status {
+    const W& w = ws[wi];
+    Plan p = plan_gemm(c->tc, w.M, w.N, Kt, true);
+    if (c->wgrad512 && p.pair && w.N % 512 == 0) {  // 256 x 512 pair tiles (MLSTM_WGRAD512)
+      p.bn = 512;
+      p.persist = false;
+    }
+    if (wi == 0 && c->overlap_now() && p.pair && p.splits == 1) {
+      // dW_h in two row halves: the first half's allreduce starts while the second computes
+      // (internal rows [0, 2h) are units [0, h/2) of every gate: 4 contiguous canonical ranges)
+      for (int half = 0; half < 2; ++half) {
+        const Opd Ah = mn(n.G5 + h + (long)half * 2 * h, 2L * h, 5L * h);
+        RET_IF(gemm<S>(c, Ah, 0, w.B, 0, 2 * h, (int)w.N, (int)Kt, p,
+                       EpiWgrad<S>{n, w.off, w.mode, (int)w.N, half * 2 * h}));
+        if (half == 0) CUDA_OR_FAIL(c, cudaEventRecordWithFlags(c->ev_wh_a, c->stream, cudaEventRecordExternal));
+      }
+    } else if (p.splits == 1 || p.pair || p.cluster) {
+      RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kt, p, EpiWgrad<S>{n, w.off, w.mode, (int)w.N}));
+    } else {
+      RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kt, p, EpiPartial{n.part, w.N, w.M * w.N}));
+      LAUNCH(c, (wgrad_finalize_kernel<S><<<grid_for(w.M * w.N), 256, 0, c->stream>>>(n, n.part, p.splits, (int)w.M,
+                                                                                        (int)w.N, w.off, w.mode)));
+    }
+    // bucket boundaries of the overlapped allreduce (external event nodes in the graph)
+    if (c->overlap_now() && wi < 3)
+      CUDA_OR_FAIL(c, cudaEventRecordWithFlags(wi == 0 ? c->ev_wh : (wi == 1 ? c->ev_wmh : c->ev_wdec), c->stream,
+                                               cudaEventRecordExternal));
+    return MLSTM_OK;
+  };
+  RET_IF(run_w(2));
   phase(c, PH_BWD);
   bool rc = false;
   if constexpr (std::is_same<S, __half>::value) rc = recur_on(c) && !c->recur_fwd_only;
@@ -1015,46 +1062,7 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
   }
   phase(c, PH_WGRAD);
   {
-    struct W {
-      Opd A, B;
-      long M, N, off;
-      int mode;
-    };
-    // every operand MN-major: the row-major [T*B][cols] stashes the recurrence wrote, K = (t, b)
-    auto mn = [&](const void* p, long cols, long ld) { return Opd{p, cols, Kt, ld, 1, 0, 0, false, true}; };
-    const W ws[4] = {
-        {mn(n.G5 + h, 4L * h, 5L * h), mn(n.Mrm, h, h), 4L * h, h, c->po.Wh, 1},      // dW_h = dZ^T M
-        {mn(n.dA, h, h), mn(n.Hrm, h, h), h, h, c->po.Wmh, 0},                         // dW_mh = dA^T H_{t-1}
-        {mn(n.dY, 256, 256), mn(n.Hrm + (long)B * h, h, h), 256, h, c->po.Wdec, 0},    // dW_dec = dY^T H
-        {mn(n.OHR, 256, 256), mn(n.G5, 5L * h, 5L * h), 256, 5L * h, 0, 2},          // S = onehot^T [dMX|dZ]
-    };
-    for (int wi = 0; wi < 4; ++wi) {
-      const W& w = ws[wi];
-      Plan p = plan_gemm(c->tc, w.M, w.N, Kt, true);
-      if (c->wgrad512 && p.pair && w.N % 512 == 0) {  // 256 x 512 pair tiles (MLSTM_WGRAD512)
-        p.bn = 512;
-        p.persist = false;
-      }
-      if (wi == 0 && c->overlap_now() && p.pair && p.splits == 1) {
-        // dW_h in two row halves: the first half's allreduce starts while the second computes
-        // (internal rows [0, 2h) are units [0, h/2) of every gate: 4 contiguous canonical ranges)
-        for (int half = 0; half < 2; ++half) {
-          const Opd Ah = mn(n.G5 + h + (long)half * 2 * h, 2L * h, 5L * h);
-          RET_IF(gemm<S>(c, Ah, 0, w.B, 0, 2 * h, (int)w.N, (int)Kt, p,
-                         EpiWgrad<S>{n, w.off, w.mode, (int)w.N, half * 2 * h}));
-          if (half == 0) CUDA_OR_FAIL(c, cudaEventRecordWithFlags(c->ev_wh_a, c->stream, cudaEventRecordExternal));
-        }
-      } else if (p.splits == 1 || p.pair || p.cluster) {
-        RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kt, p, EpiWgrad<S>{n, w.off, w.mode, (int)w.N}));
-      } else {
-        RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kt, p, EpiPartial{n.part, w.N, w.M * w.N}));
-        LAUNCH(c, (wgrad_finalize_kernel<S><<<grid_for(w.M * w.N), 256, 0, c->stream>>>(n, n.part, p.splits, (int)w.M,
-                                                                                          (int)w.N, w.off, w.mode)));
-      }
-      // bucket boundaries of the overlapped allreduce (external event nodes in the graph)
-      if (c->overlap_now() && wi < 2)
-        CUDA_OR_FAIL(c, cudaEventRecordWithFlags(wi == 0 ? c->ev_wh : c->ev_wmh, c->stream, cudaEventRecordExternal));
-    }
+    for (int wi : {0, 1, 3}) RET_IF(run_w(wi));
     // dE = S [W_mx; W_x] (M=256, N=e, K=5h) and [dW_mx; dW_x] = S^T E (M=5h, N=e, K=256)
     {
       const int sp = c->seg_splits;
@@ -1152,12 +1160,13 @@ bool wh_split_ok(mlstm_ctx* c) {
 }
 
 // The gradient allreduce's buckets as element ranges of the canonical fp16 arena,
-// in the order they are reduced, each tagged with the event it waits for: kAfterWhA = the first half of
-// dW_h (internal rows [0, 2h) = units [0, h/2) of every gate: four contiguous canonical ranges),
-// kAfterWh = dW_h, kAfterWmh = dW_mh, kAfterA = the end of graph A (E, W_mx, W_x, biases, W_dec: the
-// per-byte sums, db and the decoder gradient).  Without overlap (world 1, micro-batches, or
+// in the order they are reduced, each tagged with the event it waits for: kAfterWdec = dW_dec (run
+// before BPTT; its bucket also carries b_dec, reduced by the CE), kAfterWhA = the first half of dW_h
+// (internal rows [0, 2h) = units [0, h/2) of every gate: four contiguous canonical ranges), kAfterWh =
+// dW_h, kAfterWmh = dW_mh, kAfterA = the end of graph A (E, W_mx, W_x, b: the per-byte sums and db;
+// with weight norm the gain slots too).  Without overlap (world 1, micro-batches, or
 // MLSTM_AR_OVERLAP=0): one range, the whole arena, after graph A.
-enum { kAfterWhA = 0, kAfterWh = 1, kAfterWmh = 2, kAfterA = 3 };
+enum { kAfterWdec = 0, kAfterWhA = 1, kAfterWh = 2, kAfterWmh = 3, kAfterA = 4 };
 struct ArRange {
   int64_t off, count;
   int32_t after;
@@ -1169,6 +1178,7 @@ std::vector<ArRange> allreduce_plan(mlstm_ctx* c) {
     r.push_back({0, c->P, kAfterA});
     return r;
   }
+  r.push_back({po.Wdec, po.bdec + 256 - po.Wdec, kAfterWdec});
   const long hh = c->h;
   if (wh_split_ok<__half>(c)) {
     for (int half = 0; half < 2; ++half)
@@ -1180,7 +1190,8 @@ std::vector<ArRange> allreduce_plan(mlstm_ctx* c) {
   r.push_back({po.Wmh, po.Wx - po.Wmh, kAfterWmh});
   r.push_back({0, po.Wmh, kAfterA});
   r.push_back({po.Wx, po.Wh - po.Wx, kAfterA});
-  r.push_back({po.b, po.P - po.b, kAfterA});
+  r.push_back({po.b, po.Wdec - po.b, kAfterA});
+  if (po.P > po.bdec + 256) r.push_back({po.bdec + 256, po.P - po.bdec - 256, kAfterA});
   return r;
 }
 
@@ -1216,7 +1227,7 @@ mlstm_status run_train(mlstm_ctx* c, const uint8_t* bytes, const uint8_t* reset,
       S* a = n.arena;
       cudaStream_t cs = c->comm_stream;
       CUDA_OR_FAIL(c, cudaEventRecord(c->ev_a_end, c->stream));
-      const cudaEvent_t after_ev[4] = {c->ev_wh_a, c->ev_wh, c->ev_wmh, c->ev_a_end};
+      const cudaEvent_t after_ev[5] = {c->ev_wdec, c->ev_wh_a, c->ev_wh, c->ev_wmh, c->ev_a_end};
       const std::vector<ArRange> plan = allreduce_plan(c);
       for (size_t k = 0; k < plan.size();) {
         const int32_t after = plan[k].after;
@@ -1510,7 +1521,7 @@ mlstm_status mlstm_init(const mlstm_config* cfg, void* workspace, size_t workspa
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     if (cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi) != cudaSuccess)
       return bail(fail(MLSTM_ECUDA, "cudaStreamCreateWithPriority"));
-    for (cudaEvent_t* ev : {&c->ev_wh, &c->ev_wmh, &c->ev_a_end, &c->ev_comm, &c->ev_wh_a})
+    for (cudaEvent_t* ev : {&c->ev_wh, &c->ev_wmh, &c->ev_a_end, &c->ev_comm, &c->ev_wh_a, &c->ev_wdec})
       if (cudaEventCreateWithFlags(ev, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(MLSTM_ECUDA, "cudaEventCreate"));
   }
@@ -1898,7 +1909,7 @@ void mlstm_destroy(mlstm_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->cap) cudaStreamDestroy(c->cap);
   if (c->comm) ncclCommDestroy(c->comm);
-  for (cudaEvent_t ev : {c->ev_wh, c->ev_wmh, c->ev_a_end, c->ev_comm, c->ev_wh_a})
+  for (cudaEvent_t ev : {c->ev_wh, c->ev_wmh, c->ev_a_end, c->ev_comm, c->ev_wh_a, c->ev_wdec})
     if (ev) cudaEventDestroy(ev);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   delete c;

@@ -75,10 +75,11 @@ def test_init_argument_errors_have_no_side_effects():
                                              (4096, 4096, 2, 1024), (256, 64, 1, 0), (8192, 128, 4, 0)])
 def test_allreduce_bucket_plan(h, B, world, micro):
     """The gradient allreduce reduces every element of the canonical fp16 arena
-    exactly once, in completion order (buckets never wait on later work than the ones after them); on
-    CTA-pair plans the first W_h bucket group is units [0, h/2) of each of the four gates (contiguous
-    canonical ranges of h/2 rows), the next the other halves; W_mh follows; without overlap (one rank or
-    micro-batches) the plan is the whole arena after the backward."""
+    exactly once, in completion order (buckets never wait on later work than the ones after them): first
+    W_dec + b_dec (SURVEY 8(e) "bucket 0", computed before BPTT); on CTA-pair plans the first W_h bucket
+    group is units [0, h/2) of each of the four gates (contiguous canonical ranges of h/2 rows), the next
+    the other halves; W_mh follows; without overlap (one rank or micro-batches) the plan is the whole
+    arena after the backward."""
     cfg = M.mlstm_default_config(hidden=h, embed=64, batch=B, micro_batch=micro)
     P = M.mlstm_param_count(cfg)
     plan = M.mlstm_allreduce_plan(cfg, world)
@@ -90,16 +91,18 @@ def test_allreduce_bucket_plan(h, B, world, micro):
     afters = [a for _, _, a in plan]
     assert afters == sorted(afters)
     if world == 1 or micro:
-        assert plan == [(0, P, 3)]
+        assert plan == [(0, P, 4)]
         return
     e = 64
     off_Wh = 256 * e + h * e + h * h + 4 * h * e      # canonical offset of W_h (include/mlstm.h)
     off_Wmh = 256 * e + h * e
-    wh = [(o, c) for o, c, a in plan if a in (0, 1)]
-    if any(a == 0 for _, _, a in plan):
-        first = sorted(o for o, c, a in plan if a == 0)
+    off_Wdec = off_Wh + 4 * h * h + 4 * h
+    assert plan[0] == (off_Wdec, 256 * h + 256, 0)    # W_dec | b_dec, before the backward finishes
+    wh = [(o, c) for o, c, a in plan if a in (1, 2)]
+    if any(a == 1 for _, _, a in plan):
+        first = sorted(o for o, c, a in plan if a == 1)
         assert first == [off_Wh + g * h * h for g in range(4)]                 # gate g, units [0, h/2)
         assert all(c == (h // 2) * h for o, c in wh)
     else:
         assert wh == [(off_Wh, 4 * h * h)]
-    assert (off_Wmh, h * h, 2) in plan
+    assert (off_Wmh, h * h, 3) in plan
