@@ -137,7 +137,7 @@ struct mlstm_ctx {
   bool recur_fwd_only = false;  // recurrence = 3: persistent forward, per-timestep BPTT
   bool bwd_needs_transposes = true;  // decided while recording graph A (enqueue_train_a)
   int rc_wkm = 0;                 // MLSTM_RC_WKM=1: persistent BPTT reads the transposed (K-major) weights
-  int rc_exp = 0;                 // MLSTM_RC_EXP: timing experiments (wrong results), see RcPolicy
+  int rc_exp = 0;                 // MLSTM_RC_EXP: 64 = no per-k-block trace records (see RcPolicy::exp)
   int rc_rotate = 1;              // MLSTM_RC_ROTATE
   int rc_pf_dist = 0;             // MLSTM_RC_PF: weight k-blocks prefetched into L2 ahead of the ring
   int rc_flag_lanes = 32;  // MLSTM_RC_FLAG_LANES: activation flags acquired in parallel (1 = serial)           // decided once per ctx (shape + co-residency), see recur_on()
@@ -721,7 +721,7 @@ RcPolicy recur_policy(mlstm_ctx* c) {
   // the per-timestep activation chunks are re-read by every pair within microseconds (normal); the
   // split GEMM's weight (W_mh, 2h^2 bytes) and the segment operands (XZT / W_dec) are re-read every
   // timestep (evict_last); W_h (8h^2 bytes, more than L2) streams (evict_first unless MLSTM_L2_WH)
-  const uint32_t wide = getenv("MLSTM_RC_WNORMAL") ? 0u : (c->l2_wh > 0 ? pol_last(c->l2_wh) : kPolFirst);
+  const uint32_t wide = c->l2_wh > 0 ? pol_last(c->l2_wh) : kPolFirst;
   return RcPolicy{0u, pol_last(1.f), wide, pol_last(1.f), c->rc_flag_lanes, c->rc_pf_dist, c->rc_rotate, c->rc_exp};
 }
 

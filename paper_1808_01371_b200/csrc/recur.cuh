@@ -51,9 +51,9 @@ struct RcPolicy {  // L2 policy codes (ptx::make_policy) of the operand streams
   int pf_dist;     // weight k-blocks prefetched into L2 ahead of the ring (0 = off)
   int rotate;      // 1: each pair starts its K loop at its own chunk (spreads the L2 reads); 0: all pairs
                    // read the shared activation chunks in the same order (same lines requested together)
-  int exp;         // timing experiments only (wrong results): bit 0 = F2 A from chunk 0, bit 1 = F2 B block 0,
-                   // bit 2 = no F2 A loads, bit 3 = no F2 B loads, bit 4 = no readiness flags (races),
-                   // bit 5 = bare forward epilogue (no reduce / stores); bit 6 = no per-k-block trace records
+  int exp;         // bit 6: no per-k-block trace records (the timing experiments of round 2 --
+                   // operand substitution, skipped loads, no flags, bare epilogue -- are recorded in
+                   // profiles/r02_recur_timing_experiments.log and were removed)
 };
 
 // One operand k-block of the producer's stream: its readiness flag (null = no dependency, e.g. a
@@ -320,8 +320,7 @@ struct RcCursor {
 // each stage ran at 0.88 us per F2 k-block against 0.55 us for the two producers here.)
 template <class Dec, class IssueW, class PrefW>
 __device__ __forceinline__ void rc_weights(const RcLayout& L, int total, int pre, int per, bool leader, int pf_dist,
-                                           const RcTrace& tr, Dec dec, IssueW issue_w, PrefW prefetch_w,
-                                           bool skip_kind2 = false) {
+                                           const RcTrace& tr, Dec dec, IssueW issue_w, PrefW prefetch_w) {
   if (pf_dist > 0) {
     RcCursor pc(0, pre, per);
 #pragma unroll 1
@@ -334,12 +333,8 @@ __device__ __forceinline__ void rc_weights(const RcLayout& L, int total, int pre
   for (int wi = 0; wi < total; ++wi, c.next(pre)) {
     if (wi >= kRcStages) ptx::mbar_wait(&L.empty[s], ph);
     const RcBlk b = dec(c.u, c.i);
-    const bool skip = skip_kind2 && b.kind == 2;  // timing experiment (RcPolicy::exp bit 3)
-    if (leader) {
-      if (skip) ptx::mbar_arrive(&L.full[s]);
-      else ptx::mbar_arrive_expect_tx(&L.full[s], 2 * kRcTile);
-    }
-    if (!skip) issue_w(s, b);
+    if (leader) ptx::mbar_arrive_expect_tx(&L.full[s], 2 * kRcTile);
+    issue_w(s, b);
     if (tr.on()) tr.blk(wi, 2);
     if (pf_dist > 0 && wi + pf_dist < total) {
       prefetch_w(dec(pc.u, pc.i));
@@ -360,9 +355,8 @@ __device__ __forceinline__ void rc_weights(const RcLayout& L, int total, int pre
 // block) -- a few L2 round trips per timestep instead of one acquire + one warp barrier per block.
 template <class Dec, class IssueA>
 __device__ __forceinline__ void rc_acts(const RcLayout& L, int total, int pre, int per, int lane, bool leader,
-                                        int flag_lanes, const RcTrace& tr, Dec dec, IssueA issue_a,
-                                        bool skip_kind2 = false, bool no_flags = false) {
-  int ai = 0, known = no_flags ? total : 0;  // blocks [0, known) are published and fenced; [0, ai) issued
+                                        int flag_lanes, const RcTrace& tr, Dec dec, IssueA issue_a) {
+  int ai = 0, known = 0;  // activation blocks [0, known) are published and fenced; [0, ai) issued
   uint64_t idle_since = 0;
   RcCursor c(0, pre, per);
   int s = 0;
@@ -392,12 +386,8 @@ __device__ __forceinline__ void rc_acts(const RcLayout& L, int total, int pre, i
       for (int a = ai; a < known; ++a, c.next(pre)) {
         if (a >= kRcStages) ptx::mbar_wait(&L.empty[s], ph);
         const RcBlk b = dec(c.u, c.i);
-        const bool skip = skip_kind2 && b.kind == 2;  // timing experiment (RcPolicy::exp bit 2)
-        if (leader) {
-          if (skip) ptx::mbar_arrive(&L.full[s]);
-          else ptx::mbar_arrive_expect_tx(&L.full[s], 2 * kRcTile);
-        }
-        if (!skip) issue_a(s, b);
+        if (leader) ptx::mbar_arrive_expect_tx(&L.full[s], 2 * kRcTile);
+        issue_a(s, b);
         if (tr.on()) tr.blk(a, 3);
         if (++s == kRcStages) {
           s = 0;
@@ -489,13 +479,13 @@ __global__ void __launch_bounds__(kRcThreads, 1)
         uint8_t* dst = L.sB + s * kRcTile;
         if (b.kind == 0) ptx::tma_load_3d_2sm(dst, &tmWmh, bar0 + 8 * s, 64 * b.j, 256 * n1 + 128 * r, 0, pw1);
         else if (b.kind == 1) ptx::tma_load_3d_2sm(dst, &tmXZ, bar0 + 8 * s, 64 * b.j, 256 * p + 128 * r, 0, pws);
-        else ptx::tma_load_3d_2sm(dst, &tmWh, bar0 + 8 * s, (pol.exp & 2) ? 0 : 64 * b.j, 256 * p + 128 * r, 0, pw2);
+        else ptx::tma_load_3d_2sm(dst, &tmWh, bar0 + 8 * s, 64 * b.j, 256 * p + 128 * r, 0, pw2);
       };
       auto issue_a = [&](int s, const RcBlk& b) {
         uint8_t* dst = L.sA + s * kRcTile;
         if (b.kind == 0) ptx::tma_load_3d_2sm(dst, &tmH, bar0 + 8 * s, 64 * b.j, 128 * r, b.t, pact);
         else if (b.kind == 1) ptx::tma_load_3d_2sm(dst, &tmOH, bar0 + 8 * s, 64 * b.j, 128 * r, b.t, pact);
-        else ptx::tma_load_3d_2sm(dst, &tmM, bar0 + 8 * s, (pol.exp & 1) ? 0 : 64 * b.j, 128 * r, b.t, pact);
+        else ptx::tma_load_3d_2sm(dst, &tmM, bar0 + 8 * s, 64 * b.j, 128 * r, b.t, pact);
       };
       auto prefetch_w = [&](const RcBlk& b) {
         if (b.kind == 0) ptx::tma_prefetch_3d(&tmWmh, 64 * b.j, 256 * n1 + 128 * r, 0, pw1);
@@ -504,10 +494,9 @@ __global__ void __launch_bounds__(kRcThreads, 1)
       };
       if (warp == 0) {
         if (lane == 0)
-          rc_weights(L, T * per, 0, per, leader, pol.pf_dist, tr, dec, issue_w, prefetch_w, (pol.exp & 8) != 0);
+          rc_weights(L, T * per, 0, per, leader, pol.pf_dist, tr, dec, issue_w, prefetch_w);
       } else {
-        rc_acts(L, T * per, 0, per, lane, leader, pol.flag_lanes, tr, dec, issue_a, (pol.exp & 4) != 0,
-                (pol.exp & 16) != 0);
+        rc_acts(L, T * per, 0, per, lane, leader, pol.flag_lanes, tr, dec, issue_a);
       }
     }
   } else if (warp == 1) {
@@ -553,24 +542,6 @@ __global__ void __launch_bounds__(kRcThreads, 1)
     for (int cc = 0; cc < 2; ++cc) ld16(n.Crm + (long)b * h + 64 * p + 16 * (grp + 2 * cc), cst + 16 * cc);
 #pragma unroll 1
     for (int t = 0; t < T; ++t) {
-      if (pol.exp & 32) {  // timing experiment: bare epilogue (no reduce, no stores; wrong results)
-        ptx::mbar_wait(&L.accf[0], t & 1);
-        ptx::tc_fence_after();
-        if (tid == 0) {
-          tr.step_tag(t, 1000 + t);
-          tr.step(t, 7);
-        }
-        rc_release_acc(&L.acce[0], leader, lane);
-        rc_publish(&fM[2 * p + r], (uint32_t)(t + 1), tid);
-        if (tid == 0) tr.step(t, 9);
-        ptx::mbar_wait(&L.accf[1], t & 1);
-        ptx::tc_fence_after();
-        if (tid == 0) tr.step(t, 10);
-        rc_release_acc(&L.acce[1], leader, lane);
-        rc_publish(&fH[2 * p + r], (uint32_t)(t + 1), tid);
-        if (tid == 0) tr.step(t, 11);
-        continue;
-      }
       const int byte = n.byte_at(b, t);
       // ---------------------------------------------- F1 epilogue: split-K reduce, m = mx * a
       const float* mxp = n.tab + (long)byte * 5 * h + u1;
