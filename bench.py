@@ -312,22 +312,16 @@ def main():
         if world > 1:
             dist.barrier(device_ids=[local])
 
+    # phase events are part of the step's graphs from the first warm-up step on (profiling enabled
+    # before it), so nothing is re-recorded in the timed region; re-enabling only resets the phase
+    # accumulators, which then sum exactly the K timed steps
+    model.profile(True)
     for i in range(args.warmup):
         model.train_step(dev[i])
     launches = model.launches_per_step()
-    # per-phase times: a separate profiled run (CUDA events inside the step's graph) before the timed
-    # one, so the timed region has no phase events and no graph re-record
-    n_prof = max(1, min(args.steps, 5))
     model.profile(True)
-    model.train_step(dev[0])  # re-records the graphs with the phase events
-    for i in range(n_prof):
-        model.train_step(dev[i % args.warmup if args.warmup else 0])
     barrier()
-    phases = {k: (v[0] / n_prof, v[1]) for k, v in model.phase_times().items()}
-    model.profile(False)
-    model.train_step(dev[0])  # re-records the graphs without them
-    barrier()
-    # timed region: K steps, profiling off (no phase events, no graph re-record), one event per step
+    # timed region: K steps (one CUDA event per step on the step's stream)
     clocks = ClockSampler(local)
     clocks.start()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
@@ -347,6 +341,7 @@ def main():
         ms, med = float(tt[0].item()), float(tt[1].item())
     ms_step = ms / args.steps
     value = world * B * T / (ms_step / 1e3)
+    phases = {k: (v[0] / args.steps, v[1]) for k, v in model.phase_times().items()}
 
     # end to end through the public host entry point (pinned host bytes in, result struct out)
     e2e = None
@@ -371,11 +366,6 @@ def main():
 
     if rank != 0:
         return
-    # the profiled steps carry ~20 event records; scale their phase times to the timed step time
-    prof_total = sum(v[0] for v in phases.values())
-    scale = ms_step / prof_total if prof_total > 0 else 1.0
-    phases_raw = {k: round(v[0], 4) for k, v in phases.items()}
-    phases = {k: (v[0] * scale, v[1]) for k, v in phases.items()}
     burst, sustained, hbm, src = load_peaks()
     pf = phase_flops(h, e, B, T)
     gem = {k: phases[k] for k in pf if k in phases}
@@ -403,8 +393,8 @@ def main():
             "peak_source": f"{src} bf16_tflops_sustained (fp16 dense = bf16 dense rate)",
             "kernel": dom, "launches_per_step": nl, "gflop_per_launch": round(fl / 1e9, 3),
             "us_per_launch": round(us_launch, 2),
-            "how": f"{ph} phase {gem[ph][0]:.3f} ms/step (CUDA events in the step graph) x share {sh:.3f} "
-                   f"(ncu launch list, profiles/ncu_kernel_share.json) / {nl} launches"}
+            "how": f"{ph} phase {gem[ph][0]:.3f} ms/step (CUDA events in the step graph over the timed steps) "
+                   f"x share {sh:.3f} (ncu launch list, profiles/ncu_kernel_share.json) / {nl} launches"}
     # every GEMM phase against the same sustained peak, and the recurrences also against HBM: every
     # timestep re-streams the recurrent weights (fp16) and moves its stash rows (10h^2
     # weight bytes per timestep and direction pair; ~48h stash bytes per row per timestep)
@@ -428,9 +418,7 @@ def main():
         "roofline": roof, "roofline_phases": roof_phases,
         "step_tflops_per_gpu": whole, "step_frac_of_sustained_peak": whole / sustained,
         "phases_ms_per_step": {k: round(v[0], 4) for k, v in phases.items()},
-        "phases_profiled_ms": phases_raw,
-        "phases_from": f"profiled run of {n_prof} steps before the timed region (events in the step graph), "
-                       f"scaled by {scale:.3f} to the timed step time",
+        "phases_from": "CUDA events inside the step's graphs, summed over the K timed steps",
         "clocks": clk, "e2e": e2e, "gpu_launches": launches * args.steps,
         "loss_first_last": [results[0]["loss_nats"], results[-1]["loss_nats"]],
         "skipped_steps": int(sum(r["skipped"] for r in results)),
