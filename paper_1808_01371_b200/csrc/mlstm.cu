@@ -19,7 +19,6 @@
 #include "../../include/mlstm.h"
 #include "gemm.cuh"
 #include "kernels.cuh"
-#include "bwd_persist.cuh"
 #include "recur.cuh"
 
 using namespace mlstm;
@@ -130,7 +129,6 @@ struct mlstm_ctx {
   int force_plan = 0;          // MLSTM_FORCE_PLAN (test instrument), applied while this ctx enqueues
   bool wgrad512 = true;        // weight gradients on 256 x 512 pair tiles (MLSTM_WGRAD512=0: 256 x 256)
   bool raster_group = true;    // weight-gradient GEMMs in bands of 8 M-tiles (MLSTM_RASTER_GROUP=0: N-fastest)
-  bool bwd_persist = false;    // backward recurrence as one persistent kernel (MLSTM_BWD_PERSIST=1; measured slower)
   // persistent dataflow recurrence (recur.cuh): mlstm_config.recurrence = 1 (or MLSTM_RECUR=1)
   int recur_env = 1;
   int recur_ok = -1;
@@ -143,7 +141,6 @@ struct mlstm_ctx {
   int rc_flag_lanes = 32;  // MLSTM_RC_FLAG_LANES: activation flags acquired in parallel (1 = serial)           // decided once per ctx (shape + co-residency), see recur_on()
   float* rc_scratch = nullptr;
   uint32_t* rc_flags = nullptr;
-  uint32_t* bwd_sync = nullptr;  // its grid / split-K counters
   int async_epi = 2;  // recurrent epilogue row I/O: 0 per-thread LSU, 1 bulk copies, 2 staged + coalesced (MLSTM_ASYNC_EPI)
   bool overlap_now() const { return world > 1 && ar_overlap && nmb == 1; }
   cudaGraphExec_t gA = nullptr, gB = nullptr;
@@ -319,7 +316,6 @@ void carve(mlstm_ctx* c, Carver& cv, Net<S>& n) {
   c->part_elems = part;
   n.part = cv.take<float>(part);
   c->split_scratch = c->tc ? cv.take<float>(kSplitScratchFloats) : nullptr;
-  c->bwd_sync = cv.take<uint32_t>(kBwdSyncWords + 256);
   if (recur_shape_ok(c)) {
     c->rc_scratch = cv.take<float>(rc_scratch_floats(h));
     c->rc_flags = cv.take<uint32_t>(kRcFlagWords(h / 64));
@@ -382,7 +378,6 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   if (const char* v = getenv("MLSTM_ASYNC_EPI")) c->async_epi = atoi(v);
   if (const char* v = getenv("MLSTM_WGRAD512")) c->wgrad512 = v[0] != '0';
   if (const char* v = getenv("MLSTM_RASTER_GROUP")) c->raster_group = v[0] != '0';
-  if (const char* v = getenv("MLSTM_BWD_PERSIST")) c->bwd_persist = v[0] != '0';
   if (const char* v = getenv("MLSTM_RECUR")) c->recur_env = atoi(v);
   if (const char* v = getenv("MLSTM_RC_EXP")) c->rc_exp = atoi(v);
   if (const char* v = getenv("MLSTM_RC_WKM")) c->rc_wkm = atoi(v) != 0;
@@ -870,74 +865,6 @@ mlstm_status enqueue_forward(mlstm_ctx* c, int slot) {
   return MLSTM_OK;
 }
 
-// The persistent backward kernel applies when both per-step GEMMs take the S = 4 split-K cluster
-// plan with one resident wave (C2, C3) on the tcgen05 path; the cooperative launch guarantees
-// co-residency of the grid (it fails rather than deadlocks otherwise).
-bool bwd_persist_ok(mlstm_ctx* c) {
-  if (!c->bwd_persist || !c->tc || !c->mixed || g_force_plan != 0 || c->h % 256) return false;
-  const Plan p1 = plan_gemm(true, c->B, c->h, 4L * c->h, false), p2 = plan_gemm(true, c->B, c->h, c->h, false);
-  if (!p1.cluster || !p2.cluster || p1.splits != 4 || p2.splits != 4) return false;
-  const long ctas = 4L * (c->h / 256) * ((c->B + 127) / 128);
-  if (ctas > 148 || (ctas / 4) * 4 * 128L * 256 > kSplitScratchFloats || ctas / 4 > 256) return false;
-  static int max_clusters = -1;
-  if (max_clusters < 0) {
-    cudaFuncSetAttribute(bwd_persist_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<256>::SMEM);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(4, 1, 1);
-    cfg.blockDim = dim3(kGemmThreads);
-    cfg.dynamicSmemBytes = TcCfg<256>::SMEM;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 4;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int mc = 0;
-    max_clusters = cudaOccupancyMaxActiveClusters(&mc, bwd_persist_kernel<4>, &cfg) == cudaSuccess ? mc : 0;
-    cudaGetLastError();
-  }
-  return ctas / 4 <= max_clusters;
-}
-
-mlstm_status launch_bwd_persist(mlstm_ctx* c) {
-  Net<__half>& n = c->nh;
-  const int h = c->h, B = c->B, T = c->T;
-  const Opd dZ{n.G5 + h, B, 4L * h, 5L * h, T, 5L * B * h, kPolFirst};
-  const Opd WhT{n.WhT, h, 4L * h, 4L * h, 1, 4L * h * h, 0, true};
-  const Opd dA{n.dA, B, h, h, T, (long)B * h, kPolFirst};
-  const Opd WmhT{n.WmhT, h, h, h, 1, (long)h * h, 0, true};
-  const Opd dYs{n.dY, B, 256, 256, T, (long)B * 256, kPolFirst};
-  const Opd WdecT{n.WdecT, h, 256, 256, 1, 256L * h, 0, true};
-  const CUtensorMap *a1 = get_map(c, dZ, 128), *b1 = get_map(c, WhT, 256), *a2 = get_map(c, dA, 128),
-                    *b2 = get_map(c, WmhT, 256), *a2s = get_map(c, dYs, 128), *b2s = get_map(c, WdecT, 256);
-  if (!a1 || !b1 || !a2 || !b2 || !a2s || !b2s) {
-    c->failed = MLSTM_ECUDA;
-    return MLSTM_ECUDA;
-  }
-  CUDA_OR_FAIL(c, cudaMemsetAsync(c->bwd_sync, 0, sizeof(uint32_t) * (kBwdSyncWords + 256), c->stream));
-  CUDA_OR_FAIL(c, cudaFuncSetAttribute(bwd_persist_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       TcCfg<256>::SMEM));
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(4 * (h / 256), (B + 127) / 128, 1);
-  cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = TcCfg<256>::SMEM;
-  cfg.stream = c->stream;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 4;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeCooperative;
-  at[1].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 2;
-  CUDA_OR_FAIL(c, cudaLaunchKernelEx(&cfg, bwd_persist_kernel<4>, *a1, *b1, *a2, *b2, *a2s, *b2s, n,
-                                     c->split_scratch, c->bwd_sync));
-  count_launch(c);
-  return MLSTM_OK;
-}
-
 template <typename S>
 mlstm_status enqueue_train_a(mlstm_ctx* c) {
   Net<S>& n = net<S>(c);
@@ -1010,10 +937,9 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
   if constexpr (std::is_same<S, __half>::value) rc = recur_on(c) && !c->recur_fwd_only;
   const Plan p1 = plan_gemm(c->tc, B, h, 4 * h, false), p2 = plan_gemm(c->tc, B, h, h, false);
   const Plan p0 = plan_gemm(c->tc, B, h, 256, false);
-  const bool persist = !rc && std::is_same<S, __half>::value && bwd_persist_ok(c);
   // the per-timestep backward reads W_h, W_mh, W_dec MN-major straight from the row-major working
   // copies (no transposed copies) whenever its tile plans allow it (tensor-core path)
-  const bool bmn = c->tc && !rc && !persist && !n.dHdec && bmn_plan_ok(p0) && bmn_plan_ok(p1) && bmn_plan_ok(p2);
+  const bool bmn = c->tc && !rc && !n.dHdec && bmn_plan_ok(p0) && bmn_plan_ok(p1) && bmn_plan_ok(p2);
   c->bwd_needs_transposes = !rc && !bmn;
   const Opd WdecB = bmn ? Opd{n.Wdec_w, h, 256, h, 1, 256L * h, 0, true, true} : WdecT;
   if (rc) {
@@ -1038,8 +964,7 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
                          : Opd{n.WmhT, h, h, h, 1, (long)h * h, pol_last(c->l2_wmh), true};
     // B2 prefetches into L2 the first k-blocks (of each K split) of the W_h^T tiles B1 streams next
     const size_t es = sizeof(S);
-    if (persist) RET_IF(launch_bwd_persist(c));
-    for (int t = (persist || rc) ? -1 : T - 1; t >= 0; --t) {
+    for (int t = rc ? -1 : T - 1; t >= 0; --t) {
       // B1(t) prefetches what B2's gate backward of step t-1 reads (written long ago by the
       // forward: gates, c_{t-1} and c_{t-2} (adjacent blocks), dH_dec); B2 prefetches the a-stash
       // block the next B1 reads.

@@ -397,22 +397,6 @@ def test_forced_tile_plans_match_oracle(plan, h, B, T, monkeypatch):
     assert np.isfinite(nats) and tokens == B * T
 
 
-@pytest.mark.parametrize("h,B,T", [(1024, 128, 6), (1024, 200, 3)])
-def test_persistent_backward_matches_oracle(h, B, T, monkeypatch):
-    """The backward recurrence as one persistent cooperative kernel (MLSTM_BWD_PERSIST=1: grid-wide
-    phase barriers, split-K counters in global memory) against the oracle; B=200 is ragged."""
-    monkeypatch.setenv("MLSTM_BWD_PERSIST", "1")
-    e = 64
-    m = make_model(h, e, B, T, "mixed")
-    theta0 = oracle_theta(h, e)
-    by = inputs(B, T)
-    res = m.train_step(to_dev(by))
-    loss_ref, g_ref, (hT, cT), _ = oracle_step(theta0, by, h, e)
-    assert abs(res["loss_nats"] - loss_ref) / loss_ref <= TOL["mixed"]["loss_rel"]
-    rep = compare_grads(m.get_grads().astype(np.float64), g_ref, h, e, "mixed")
-    assert min(rep.values()) >= TOL["mixed"]["grad_cos"], rep
-
-
 def test_multi_step_trace_mixed_tracks_oracle():
     """10 mixed-precision steps at C2's width (fp16 storage, loss scaling, Adam on fp32 masters)
     against the fp64 oracle loop: the loss stays within the north_star bound at every step."""
