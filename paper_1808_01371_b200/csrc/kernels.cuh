@@ -423,9 +423,24 @@ struct EpiWgrad {
   int mode;
   int N;
   int row0 = 0;  // first output row of this launch (dW_h split into row halves for the allreduce)
+  const float* acc = nullptr;  // fp32 partial of the K range the side stream reduced (EpiWacc), added first
   template <int NG>
-  __device__ __forceinline__ void run(int row_, int col0, const float* v) const {
+  __device__ __forceinline__ void run(int row_, int col0, const float* v_) const {
     const int row = row_ + row0;
+    float w[16 * NG];
+    const float* v = v_;
+    if (acc) {
+      const float4* a = reinterpret_cast<const float4*>(acc + (long)row * N + col0);
+#pragma unroll
+      for (int q = 0; q < 4 * NG; ++q) {
+        const float4 x = a[q];
+        w[4 * q] = v_[4 * q] + x.x;
+        w[4 * q + 1] = v_[4 * q + 1] + x.y;
+        w[4 * q + 2] = v_[4 * q + 2] + x.z;
+        w[4 * q + 3] = v_[4 * q + 3] + x.w;
+      }
+      v = w;
+    }
     if (mode == 2) {
       float* dst = n.Scan + (long)row * 5 * n.h;
 #pragma unroll
@@ -440,6 +455,33 @@ struct EpiWgrad {
 #pragma unroll
     for (int i = 0; i < 16 * NG; ++i) bad |= s_nonfinite<S>(v[i]);
     if (bad) n.st->overflow = 1;
+  }
+};
+
+// fp32 partial of a weight gradient over one K range (a chunk of timesteps), reduced on the side stream
+// while the backward recurrence still runs: [M][N] internal rows, the first chunk stores, later ones add
+// (the side stream runs them in order); EpiWgrad adds the result to the remaining K range's sum.
+struct EpiWacc {
+  static constexpr int kMinGroups = 1;
+  __device__ __forceinline__ void operator()(int row, int col0, float (&v)[64]) const { run<4>(row, col0, v); }
+  float* part;
+  int N;
+  int first;
+  template <int NG>
+  __device__ __forceinline__ void run(int row, int col0, const float* v) const {
+    float4* d = reinterpret_cast<float4*>(part + (long)row * N + col0);
+#pragma unroll
+    for (int q = 0; q < 4 * NG; ++q) {
+      float4 x = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      if (!first) {
+        const float4 o = d[q];
+        x.x += o.x;
+        x.y += o.y;
+        x.z += o.z;
+        x.w += o.w;
+      }
+      d[q] = x;
+    }
   }
 };
 

@@ -40,6 +40,7 @@ template <> struct EpiTag<EpiPartial> { static constexpr int value = 9; };
 template <class E> constexpr bool kMNEpi = false;
 template <typename S> constexpr bool kMNEpi<EpiWgrad<S>> = true;
 template <> constexpr bool kMNEpi<EpiPartial> = true;
+template <> constexpr bool kMNEpi<EpiWacc> = true;
 // epilogues of the backward recurrence's GEMMs, whose B operand (a weight) may be read MN-major
 // straight from its row-major working copy (K-major A, MN-major B)
 template <class E> constexpr bool kBMNEpi = false;
@@ -129,6 +130,15 @@ struct mlstm_ctx {
   int force_plan = 0;          // MLSTM_FORCE_PLAN (test instrument), applied while this ctx enqueues
   bool wgrad512 = true;        // weight gradients on 256 x 512 pair tiles (MLSTM_WGRAD512=0: 256 x 256)
   bool raster_group = true;    // weight-gradient GEMMs in bands of 8 M-tiles (MLSTM_RASTER_GROUP=0: N-fastest)
+  // dW_h over the last side_chunks x side_ch timesteps on a low-priority side stream, on side_pairs CTA
+  // pairs, while the per-timestep backward recurrence (128 CTAs) still runs (MLSTM_WGRAD_SIDE=chunks[,ch[,pairs]])
+  int side_chunks = 0, side_ch = 32, side_pairs = 10, side_pol = 1;  // side_pol 1: operands evict_first
+  cudaStream_t side = nullptr;
+  cudaEvent_t side_ev[17] = {};  // [0, side_chunks): chunk j's dZ rows are final; [16]: side stream done
+  float* wpart = nullptr;        // fp32 [4h][h] partial of dW_h over the side chunks
+  int tc2p_pairs = 0;            // > 0: grid of the persistent pair engine for the launch being enqueued
+  int prio = 0;                  // launch priority attribute of the GEMM being enqueued (0: none)
+  int prio_hi = 0, prio_lo = 0;
   // persistent dataflow recurrence (recur.cuh): mlstm_config.recurrence = 1 (or MLSTM_RECUR=1)
   int recur_env = 1;
   int recur_ok = -1;
@@ -378,6 +388,14 @@ void set_dims(mlstm_ctx* c, const mlstm_config* cfg) {
   if (const char* v = getenv("MLSTM_ASYNC_EPI")) c->async_epi = atoi(v);
   if (const char* v = getenv("MLSTM_WGRAD512")) c->wgrad512 = v[0] != '0';
   if (const char* v = getenv("MLSTM_RASTER_GROUP")) c->raster_group = v[0] != '0';
+  if (const char* v = getenv("MLSTM_WGRAD_SIDE")) {
+    int a = 0, b = 32, d = 10, q = 1;
+    sscanf(v, "%d,%d,%d,%d", &a, &b, &d, &q);
+    c->side_pol = q;
+    c->side_chunks = std::max(0, std::min(16, a));
+    c->side_ch = std::max(1, b);
+    c->side_pairs = std::max(1, std::min(74, d));
+  }
   if (const char* v = getenv("MLSTM_RECUR")) c->recur_env = atoi(v);
   if (const char* v = getenv("MLSTM_RC_EXP")) c->rc_exp = atoi(v);
   if (const char* v = getenv("MLSTM_RC_WKM")) c->rc_wkm = atoi(v) != 0;
@@ -461,7 +479,7 @@ cudaError_t launch_gemm(mlstm_ctx* c, Kern kern, dim3 grid, int smem, int cluste
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = c->stream;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   int na = 0;
   if (cluster > 1) {
     at[na].id = cudaLaunchAttributeClusterDimension;
@@ -473,6 +491,11 @@ cudaError_t launch_gemm(mlstm_ctx* c, Kern kern, dim3 grid, int smem, int cluste
   if (c->pdl) {
     at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (c->prio != 0) {  // graph nodes keep it (instantiated with cudaGraphInstantiateFlagUseNodePriority)
+    at[na].id = cudaLaunchAttributePriority;
+    at[na].val.priority = c->prio;
     ++na;
   }
   cfg.attrs = at;
@@ -519,7 +542,7 @@ cudaError_t launch_tc2p(mlstm_ctx* c, const CUtensorMap* ma, const CUtensorMap* 
                         const CUtensorMap* mb2, Seg2 sg, int M, int N, int K, int az, int bz, uint32_t pa,
                         uint32_t pb, int flags, PrefetchJob pj, const Epi& epi) {
   const int tiles = ((M + 255) / 256) * ((N + BN - 1) / BN);
-  const int npairs = std::min(tiles, g_max_pairs);
+  const int npairs = std::min(tiles, c->tc2p_pairs > 0 ? c->tc2p_pairs : g_max_pairs);
   return launch_gemm(c, gemm_tc2p_kernel<BN, Epi, MN>, dim3(2 * npairs, 1, 1), Tc2Cfg<BN>::SMEM, 2, *ma, *mb, *ma2,
                      *mb2, sg, M, N, K, az, bz, 0, pa, pb, flags, pj, epi);
 }
@@ -901,10 +924,28 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
       {mn(n.dY, 256, 256), mn(n.Hrm + (long)B * h, h, h), 256, h, c->po.Wdec, 0},    // dW_dec = dY^T H
       {mn(n.OHR, 256, 256), mn(n.G5, 5L * h, 5L * h), 256, 5L * h, 0, 2},          // S = onehot^T [dMX|dZ]
   };
+  // dW_h side chunks (MLSTM_WGRAD_SIDE): chunk j = timesteps [T - (j+1) ch, T - j ch), reduced on the side
+  // stream as soon as the backward has produced its dZ rows; dW_h's main GEMM then covers K = [0, Kmain)
+  // and adds the side partial in its epilogue
+  int nside = 0;
+  if constexpr (std::is_same<S, __half>::value) {
+    const int ch = c->side_ch;
+    if (c->side_chunks > 0 && c->tc && !n.dHdec && !(recur_on(c) && !c->recur_fwd_only) && h % 256 == 0)
+      nside = std::max(0, std::min(c->side_chunks, (T - 1) / ch));
+    const Plan pm = plan_gemm(c->tc, 4L * h, h, (long)(T - nside * ch) * B, true);
+    if (!(pm.splits == 1 || pm.pair || pm.cluster)) nside = 0;  // the split-K finaliser has no partial input
+  }
+  const long Kmain = (long)(T - nside * c->side_ch) * B;
   // one weight-gradient job (plan, optional dW_h row halves, split-K finaliser, bucket event)
   auto run_w = [&](int wi) -> mlstm_status {
-    const W& w = ws[wi];
-    Plan p = plan_gemm(c->tc, w.M, w.N, Kt, true);
+    W w = ws[wi];
+    const long Kw = (wi == 0) ? Kmain : Kt;
+    const float* acc = (wi == 0 && nside > 0) ? c->wpart : nullptr;
+    if (wi == 0) {
+      w.A.K = Kw;
+      w.B.K = Kw;
+    }
+    Plan p = plan_gemm(c->tc, w.M, w.N, Kw, true);
     if (c->wgrad512 && p.pair && w.N % 512 == 0) {  // 256 x 512 pair tiles (MLSTM_WGRAD512)
       p.bn = 512;
       p.persist = false;
@@ -913,14 +954,17 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
       // dW_h in two row halves: the first half's allreduce starts while the second computes
       // (internal rows [0, 2h) are units [0, h/2) of every gate: 4 contiguous canonical ranges)
       for (int half = 0; half < 2; ++half) {
-        const Opd Ah = mn(n.G5 + h + (long)half * 2 * h, 2L * h, 5L * h);
-        RET_IF(gemm<S>(c, Ah, 0, w.B, 0, 2 * h, (int)w.N, (int)Kt, p,
-                       EpiWgrad<S>{n, w.off, w.mode, (int)w.N, half * 2 * h}));
+        Opd Ah = mn(n.G5 + h + (long)half * 2 * h, 2L * h, 5L * h);
+        Ah.K = Kw;
+        RET_IF(gemm<S>(c, Ah, 0, w.B, 0, 2 * h, (int)w.N, (int)Kw, p,
+                       EpiWgrad<S>{n, w.off, w.mode, (int)w.N, half * 2 * h, acc}));
         if (half == 0) CUDA_OR_FAIL(c, cudaEventRecordWithFlags(c->ev_wh_a, c->stream, cudaEventRecordExternal));
       }
     } else if (p.splits == 1 || p.pair || p.cluster) {
-      RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kt, p, EpiWgrad<S>{n, w.off, w.mode, (int)w.N}));
+      RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kw, p,
+                     EpiWgrad<S>{n, w.off, w.mode, (int)w.N, 0, acc}));
     } else {
+      if (acc) return fail(MLSTM_EINVAL, "wgrad side chunks need a single-pass dW_h plan");
       RET_IF(gemm<S>(c, w.A, 0, w.B, 0, (int)w.M, (int)w.N, (int)Kt, p, EpiPartial{n.part, w.N, w.M * w.N}));
       LAUNCH(c, (wgrad_finalize_kernel<S><<<grid_for(w.M * w.N), 256, 0, c->stream>>>(n, n.part, p.splits, (int)w.M,
                                                                                         (int)w.N, w.off, w.mode)));
@@ -932,6 +976,31 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
     return MLSTM_OK;
   };
   RET_IF(run_w(2));
+  // side chunk j of dW_h: fork from the capture stream once its dZ rows exist, run on side_pairs pairs
+  // at the lowest priority (the recurrence's GEMMs carry the highest)
+  auto enqueue_side = [&](int j) -> mlstm_status {
+    const long lo = (long)T - (long)(j + 1) * c->side_ch, Kc = (long)c->side_ch * B;
+    CUDA_OR_FAIL(c, cudaEventRecord(c->side_ev[j], c->stream));
+    CUDA_OR_FAIL(c, cudaStreamWaitEvent(c->side, c->side_ev[j], 0));
+    const uint32_t pol = c->side_pol ? kPolFirst : 0;  // keep the recurrence's L2-resident weights
+    const Opd A{n.G5 + h + lo * B * 5L * h, 4L * h, Kc, 5L * h, 1, 0, pol, false, true};
+    const Opd Bm{n.Mrm + lo * B * (long)h, h, Kc, h, 1, 0, pol, false, true};
+    cudaStream_t keep = c->stream;
+    const bool pdl = c->pdl;
+    const int prio = c->prio;
+    c->stream = c->side;
+    c->pdl = false;
+    c->prio = 0;
+    c->tc2p_pairs = c->side_pairs;
+    const mlstm_status r =
+        gemm<S>(c, A, 0, Bm, 0, 4 * h, h, (int)Kc, Plan{256, 1, true, false, true}, EpiWacc{c->wpart, h, j == 0});
+    c->stream = keep;
+    c->pdl = pdl;
+    c->prio = prio;
+    c->tc2p_pairs = 0;
+    return r;
+  };
+  if (nside > 0) c->prio = c->prio_hi;
   phase(c, PH_BWD);
   bool rc = false;
   if constexpr (std::is_same<S, __half>::value) rc = recur_on(c) && !c->recur_fwd_only;
@@ -983,10 +1052,18 @@ mlstm_status enqueue_train_a(mlstm_ctx* c) {
         RET_IF(gemm<S>(c, dZ, t, WhT, 0, B, h, 4 * h, p1, EpiB1<S>{n, t}, pb1));
       segd.az2 = t - 1;
       if (t > 0) RET_IF(gemm<S>(c, dA, t, WmhT, 0, B, h, h, p2, EpiB2<S>{n, t - 1}, pb2, segd));
+      const int done = T - (t - 1);  // timesteps [t-1, T) have their dZ rows now
+      if (nside > 0 && t > 0 && done % c->side_ch == 0 && done / c->side_ch <= nside)
+        RET_IF(enqueue_side(done / c->side_ch - 1));
     }
   }
+  c->prio = 0;
   phase(c, PH_WGRAD);
   {
+    if (nside > 0) {  // join the side stream: dW_h's main GEMM adds its partial
+      CUDA_OR_FAIL(c, cudaEventRecord(c->side_ev[16], c->side));
+      CUDA_OR_FAIL(c, cudaStreamWaitEvent(c->stream, c->side_ev[16], 0));
+    }
     for (int wi : {0, 1, 3}) RET_IF(run_w(wi));
     // dE = S [W_mx; W_x] (M=256, N=e, K=5h) and [dW_mx; dW_x] = S^T E (M=5h, N=e, K=256)
     {
@@ -1046,7 +1123,7 @@ mlstm_status record_graph(mlstm_ctx* c, mlstm_status (*fn)(mlstm_ctx*), cudaGrap
     return s;
   }
   CUDA_OR_FAIL(c, e);
-  CUDA_OR_FAIL(c, cudaGraphInstantiate(out, g, 0));
+  CUDA_OR_FAIL(c, cudaGraphInstantiate(out, g, c->side_chunks > 0 ? cudaGraphInstantiateFlagUseNodePriority : 0));
   cudaGraphDestroy(g);
   return MLSTM_OK;
 }
@@ -1421,6 +1498,16 @@ mlstm_status mlstm_init(const mlstm_config* cfg, void* workspace, size_t workspa
       return bail(fail(MLSTM_ECUDA, "cudaEventCreate"));
   if (cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(MLSTM_ECUDA, "cudaStreamCreate"));
+  if (c->side_chunks > 0) {
+    cudaDeviceGetStreamPriorityRange(&c->prio_lo, &c->prio_hi);
+    if (cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, c->prio_lo) != cudaSuccess)
+      return bail(fail(MLSTM_ECUDA, "cudaStreamCreateWithPriority"));
+    for (cudaEvent_t& ev : c->side_ev)
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+        return bail(fail(MLSTM_ECUDA, "cudaEventCreate"));
+    if (cudaMalloc(&c->wpart, sizeof(float) * 4 * (size_t)c->h * c->h) != cudaSuccess)
+      return bail(fail(MLSTM_ECUDA, "cudaMalloc wpart"));
+  }
   for (int i = 0; i <= NPH; ++i)
     if (cudaEventCreate(&c->ev[i]) != cudaSuccess) return bail(fail(MLSTM_ECUDA, "cudaEventCreate"));
   // zero everything (pads of the transposed stashes must stay zero), then init
@@ -1837,6 +1924,10 @@ void mlstm_destroy(mlstm_ctx* c) {
   for (cudaEvent_t ev : {c->ev_wh, c->ev_wmh, c->ev_a_end, c->ev_comm, c->ev_wh_a, c->ev_wdec})
     if (ev) cudaEventDestroy(ev);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->side) cudaStreamDestroy(c->side);
+  for (cudaEvent_t ev : c->side_ev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->wpart) cudaFree(c->wpart);
   delete c;
 }
 
