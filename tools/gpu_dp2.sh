@@ -1,0 +1,9 @@
+#!/bin/bash
+# 2 GPUs: the NCCL data-parallel tests and the C3 N=2 bench line
+cd "$GRAFT_REPO_ROOT"
+O=gpurun_out/dp2f; mkdir -p $O
+timeout 1200 python -m pytest -q -m gpu tests/test_gpu_dp.py > $O/tests.log 2>&1
+echo "tests exit $?" >> $O/tests.log
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 \
+  bench.py --gpus 2 > $O/bench_n2.log 2>&1
+echo "exit $?" >> $O/bench_n2.log
