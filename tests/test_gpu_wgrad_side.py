@@ -12,12 +12,12 @@ from gpu_helpers import TOL, compare_grads, inputs, make_model, oracle_step, ora
 pytestmark = pytest.mark.gpu
 
 
-def _step(monkeypatch, side, h, e, B, T, recurrence=2):
+def _step(monkeypatch, side, h, e, B, T, recurrence=2, **kw):
     if side:
         monkeypatch.setenv("MLSTM_WGRAD_SIDE", side)
     else:
         monkeypatch.delenv("MLSTM_WGRAD_SIDE", raising=False)
-    m = make_model(h, e, B, T, "mixed", recurrence=recurrence)
+    m = make_model(h, e, B, T, "mixed", recurrence=recurrence, **kw)
     r = m.train_step(to_dev(inputs(B, T)))
     g = m.get_grads().astype(np.float64)
     m.close()
@@ -39,14 +39,17 @@ def test_side_chunks_match_oracle(monkeypatch, h, B, T, side, recurrence):
         assert v >= TOL["mixed"]["grad_cos"], (n, v, rep)
 
 
-@pytest.mark.parametrize("h,B,T,side", [(1024, 16, 16, "3,4,3"), (4096, 256, 8, "1,4,10")])
-def test_side_chunks_change_only_dW_h_summation_order(monkeypatch, h, B, T, side):
+@pytest.mark.parametrize("h,B,T,side,micro", [(1024, 16, 16, "3,4,3", 0), (4096, 256, 8, "1,4,10", 0),
+                                               (512, 64, 12, "2,5,2", 16)])
+def test_side_chunks_change_only_dW_h_summation_order(monkeypatch, h, B, T, side, micro):
     """Against the same step without side chunks: every other gradient bitwise equal (the side stream
     writes nothing else), dW_h within one fp16 rounding (rel 2^-9; abs 1e-3 of the largest entry where
-    the sum cancels) -- also at the C3 width and rows per GPU."""
+    the sum cancels) -- also at the C3 width and rows per GPU, and with micro-batches (each pass of the
+    step's graph A forks and joins its own side chunks; the fp32 accumulation across passes follows)."""
     e = 64
-    r0, g0 = _step(monkeypatch, None, h, e, B, T)
-    r1, g1 = _step(monkeypatch, side, h, e, B, T)
+    kw = {"micro_batch": micro} if micro else {}
+    r0, g0 = _step(monkeypatch, None, h, e, B, T, **kw)
+    r1, g1 = _step(monkeypatch, side, h, e, B, T, **kw)
     assert r0["loss_nats"] == r1["loss_nats"]
     G0, G1 = split(g0, h, e), split(g1, h, e)
     for n in G0:
@@ -58,3 +61,4 @@ def test_side_chunks_change_only_dW_h_summation_order(monkeypatch, h, B, T, side
     # fp32 sums in another order: one fp16 rounding apart, or a few ulps where the sum cancels
     bad = np.abs(a - b) > 2.0 ** -9 * np.abs(b) + 1e-3 * scale
     assert not bad.any(), (int(bad.sum()), float(np.abs(a - b).max()), scale)
+
