@@ -131,7 +131,8 @@ struct mlstm_ctx {
   bool wgrad512 = true;        // weight gradients on 256 x 512 pair tiles (MLSTM_WGRAD512=0: 256 x 256)
   bool raster_group = true;    // weight-gradient GEMMs in bands of 8 M-tiles (MLSTM_RASTER_GROUP=0: N-fastest)
   // dW_h over the last side_chunks x side_ch timesteps on a low-priority side stream, on side_pairs CTA
-  // pairs, while the per-timestep backward recurrence (128 CTAs) still runs (MLSTM_WGRAD_SIDE=chunks[,ch[,pairs]])
+  // pairs, while the per-timestep backward recurrence (128 CTAs) still runs
+  // (MLSTM_WGRAD_SIDE=chunks[,ch[,pairs[,pol]]]; measured a wash under the power cap, DESIGN 9.1: off by default)
   int side_chunks = 0, side_ch = 32, side_pairs = 10, side_pol = 1;  // side_pol 1: operands evict_first
   cudaStream_t side = nullptr;
   cudaEvent_t side_ev[17] = {};  // [0, side_chunks): chunk j's dZ rows are final; [16]: side stream done
