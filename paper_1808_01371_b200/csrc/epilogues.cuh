@@ -177,15 +177,32 @@ struct EpiF2IO : EpiF2<S> {
     ptx::bulk_g2s(io.buf + slot * kSlot + kCp + io.lane * 80, n.Crm + ((long)this->t * n.B + b) * n.h + j0, 64,
                   io.bar);
   }
+  // c_{t-1} of this lane's row and chunk straight into registers (issued by the epilogue warps while the
+  // main loop still runs; c_{t-1} was written two launches earlier, see gemm_tc2_kernel)
+  static constexpr bool kPreC = true;
+  __device__ __forceinline__ void preload_c(const EpiIO& io, int col0, float4 (&c)[4]) const {
+    const Net<S>& n = this->n;
+    if (!io.valid()) return;
+    const float4* src =
+        reinterpret_cast<const float4*>(n.Crm + ((long)this->t * n.B + io.row0 + io.lane) * n.h + (col0 >> 6) * 16);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = src[k];
+  }
   template <int NG>
   __device__ __forceinline__ void run_io(const EpiIO& io, int slot, int col0, const float* v) const {
+    ptx::mbar_wait(io.bar, 0);
+    const float4* cp = reinterpret_cast<const float4*>(io.buf + slot * kSlot + kCp + io.lane * 80);
+    const float4 c[4] = {cp[0], cp[1], cp[2], cp[3]};
+    run_io_c<NG>(io, slot, col0, v, c);
+  }
+  template <int NG>
+  __device__ __forceinline__ void run_io_c(const EpiIO& io, int slot, int col0, const float* v,
+                                           const float4 (&cp)[4]) const {
     static_assert(NG == 4, "one call = 4 gates x 16 units");
     const Net<S>& n = this->n;
     const int h = n.h, t = this->t, j0 = (col0 >> 6) * 16, lane = io.lane;
     const int b = io.row0 + lane;
     uint8_t* sb = io.buf + slot * kSlot;
-    ptx::mbar_wait(io.bar, 0);
-    const float4* cp = reinterpret_cast<const float4*>(sb + kCp + lane * 80);
     __align__(16) S gs[64];
     __align__(16) float cv[16];
     __align__(16) S hv[16];

@@ -61,6 +61,15 @@ struct HasTile<E, decltype(void(E::kTile))> {
 };
 
 template <class E, class = void>
+struct HasPreC {  // row-I/O epilogue whose per-row input can be loaded into registers before the accumulator
+  static constexpr bool value = false;
+};
+template <class E>
+struct HasPreC<E, decltype(void(E::kPreC))> {
+  static constexpr bool value = E::kPreC;
+};
+
+template <class E, class = void>
 struct HasAsyncIO {
   static constexpr bool value = false;
 };
@@ -79,6 +88,9 @@ struct TcCfg {  // one CTA per 128 x BN tile
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 512;
   static_assert(STAGES * STAGE_BYTES >= kEpiWarps * kWarpStageBytes, "epilogue staging windows");
 };
+#ifndef MLSTM_F2_PREC
+#define MLSTM_F2_PREC 1  // F2 epilogue: c_{t-1} into registers during the main loop (0: bulk copy after it)
+#endif
 #ifndef MLSTM_TC2_STAGES256
 #define MLSTM_TC2_STAGES256 6  // ring depth of the 256 x 256 CTA-pair tiles (A/B builds override)
 #endif
@@ -423,6 +435,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if constexpr (HasTile<Epi>::value) {
       epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
       tile_epilogue<BN>(L, tmem, nkb > 0, m0, n0, M, N, epi);
+    } else if constexpr (HasPreC<Epi>::value && MLSTM_F2_PREC) {
+      // the epilogue's per-row input (F2: c_{t-1}) is loaded into registers while the main loop runs,
+      // so no load latency sits between the accumulator and the outputs
+      const EpiIO io = L.io(warp - 2, m0 + q * 32, M, lane);
+      constexpr int NC = (BN / 64 + 1) / 2;  // chunks per epilogue warp (c = grp, grp + 2, ...)
+      float4 cpre[NC][4];
+      ptx::pdl_wait();
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        const int c = grp + 2 * i;
+        if (c < BN / 64 && n0 + c * 64 < N) epi.preload_c(io, n0 + c * 64, cpre[i]);
+      }
+      epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        const int c = grp + 2 * i;
+        if (c >= BN / 64) break;
+        float v[64];
+        tmem_chunk(tmem, q, c, nkb > 0, v);
+        const int col0 = n0 + c * 64;
+        if (col0 < N) epi.template run_io_c<4>(io, i, col0, v, cpre[i]);
+      }
+      ptx::bulk_wait_read0();
     } else if constexpr (HasAsyncIO<Epi>::value) {
       const EpiIO io = L.io(warp - 2, m0 + q * 32, M, lane);
       epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
@@ -511,6 +546,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     if constexpr (HasTile<Epi>::value) {
       epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
       tile_epilogue<BN>(L, tmem, nkb > 0, m0, n0, M, N, epi);
+    } else if constexpr (HasPreC<Epi>::value && MLSTM_F2_PREC) {
+      // the epilogue's per-row input (F2: c_{t-1}) is loaded into registers while the main loop runs,
+      // so no load latency sits between the accumulator and the outputs
+      const EpiIO io = L.io(warp - 2, m0 + q * 32, M, lane);
+      constexpr int NC = (BN / 64 + 1) / 2;  // chunks per epilogue warp (c = grp, grp + 2, ...)
+      float4 cpre[NC][4];
+      ptx::pdl_wait();
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        const int c = grp + 2 * i;
+        if (c < BN / 64 && n0 + c * 64 < N) epi.preload_c(io, n0 + c * 64, cpre[i]);
+      }
+      epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        const int c = grp + 2 * i;
+        if (c >= BN / 64) break;
+        float v[64];
+        tmem_chunk(tmem, q, c, nkb > 0, v);
+        const int col0 = n0 + c * 64;
+        if (col0 < N) epi.template run_io_c<4>(io, i, col0, v, cpre[i]);
+      }
+      ptx::bulk_wait_read0();
     } else if constexpr (HasAsyncIO<Epi>::value) {
       const EpiIO io = L.io(warp - 2, m0 + q * 32, M, lane);
       epi_begin(L.accf, nkb > 0, MLSTM_TRACE_SLOT(3));
